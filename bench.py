@@ -1,0 +1,418 @@
+"""Benchmark of the B200 snapshot path (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg2] [--mode ring|direct|zerocopy]
+
+Metric (BASELINE.json): checkpoint GB/s per GPU and per box, and training-blocked
+ms per checkpoint. One step = one lazy checkpoint of this rank's state of the
+named config (default cfg2: Llama-2 7B, ZeRO-1 over 8 ranks; rank r snapshots
+shard r), i.e. update (pattern kernel rewrites every state byte) -> issue ->
+snapshot complete (all bytes in pinned host memory) -> checksums complete.
+Inputs (the state) live in HBM and are larger than L2. Multi-GPU: one process
+per GPU, each snapshots its own shard (no data-path collective), value = all
+ranks' bytes / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PCIE_D2H_MEASURED_GBPS = 57.2  # pinned cudaMemcpy D2H on this pool's B200 (gpurun_out/probe_box.json)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device: int):
+        self.samples = []
+        self.dev = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=clocks.sm,clocks.max.sm,utilization.gpu,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[4:8]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def sample_recipe(cfg: str, rank: int, max_raw: int = 8):
+    """Bounded sample of the workload for the CPU reference: the first `max_raw`
+    raw objects of this rank (+ its metadata), same sizes and patterns."""
+    from paper_2601_16956_b200 import synthetic as S
+
+    rec = S.config_recipe(cfg, rank)
+    r = rec.ranks[0]
+    raws = [o for o in r.objects if o.kind == 0][:max_raw]
+    metas = [o for o in r.objects if o.kind == 1 and o.meta[0] == "meta"]
+    r.objects = raws + metas
+    return rec
+
+
+def run_reference(args, sample_max_raw=8, steps=None, warmup=None):
+    """The reference CPU implementation (oracle/_ref/ts_ref_driver, built from
+    /root/reference) on a bounded sample of this config, one process, its default
+    4 flush workers + 1 copier thread, files to /dev/shm."""
+    drv = os.path.join(ROOT, "oracle", "_ref", "ts_ref_driver")
+    if not os.path.exists(drv):
+        return None
+    rec = sample_recipe(args.config, 0, sample_max_raw)
+    sample_bytes = rec.ranks[0].raw_bytes
+    tmp = tempfile.mkdtemp(dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
+    try:
+        rp = os.path.join(tmp, "sample.recipe")
+        with open(rp, "w") as f:
+            f.write(rec.to_text())
+        cap = 1 << (max(sample_bytes, 256 << 20) - 1).bit_length()
+        cmd = [drv, "bench", rp, os.path.join(tmp, "ckpt"), "--workers", "4", "--cache", str(cap),
+               "--reps", str(steps if steps is not None else 1), "--warmup",
+               str(warmup if warmup is not None else 0)]
+        out = subprocess.run(cmd, capture_output=True, text=True, check=True).stdout
+        rows = [json.loads(l) for l in out.splitlines() if l.startswith("{")]
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+    timed = [r for r in rows if not r["warmup"]]
+    snap = sum(r["snapshot_s"] for r in timed)
+    pers = sum(r["persist_s"] for r in timed)
+    b = sum(r["bytes"] for r in timed)
+    return {"value": b / snap / 1e9, "persist_gbps": b / pers / 1e9, "steps": len(timed),
+            "bytes_per_step": timed[0]["bytes"], "snapshot_s": [r["snapshot_s"] for r in timed],
+            "issue_ms": [1e3 * r["issue_s"] for r in timed],
+            "sample": f"{args.config} rank 0: first {sample_max_raw} raw objects + metadata "
+                      f"({timed[0]['bytes'] / 1e9:.2f} GB), lazy, 4 flush workers, files on /dev/shm"}
+
+
+def reference_arm(args):
+    ws, rank, _ = dist_info()
+    if rank != 0:
+        return
+    r = run_reference(args, steps=args.steps, warmup=args.warmup)
+    if r is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ts_ref_driver not built"}))
+        return
+    line = {"metric": "checkpoint snapshot GB/s (per GPU / box)", "impl": "reference", "value": round(r["value"], 4),
+            "unit": "GB/s", "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
+            "ms_per_step": round(1e3 * statistics.mean(r["snapshot_s"]), 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": args.config + " (bounded CPU sample)", "sample": r["sample"]},
+            "persist_gbps": round(r["persist_gbps"], 4), "blocked_ms": round(statistics.mean(r["issue_ms"]), 3),
+            "cpu_baseline": {"value": round(r["value"], 4), "unit": "GB/s", "cores": 5, "kind": "reference",
+                             "sample": r["sample"]},
+            "e2e": {"value": round(r["value"], 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def gemm_load(ms: float, dev):
+    """Synthetic forward/backward: back-to-back bf16 GEMMs for ~ms milliseconds."""
+    import torch
+
+    n = 8192
+    a = torch.randn(n, n, device=dev, dtype=torch.bfloat16)
+    b = torch.randn(n, n, device=dev, dtype=torch.bfloat16)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(3):
+        a @ b
+    e0.record()
+    for _ in range(10):
+        a @ b
+    e1.record()
+    e1.synchronize()
+    per = e0.elapsed_time(e1) / 10
+    reps = max(1, int(ms / per))
+
+    def run():
+        c = None
+        for _ in range(reps):
+            c = a @ b
+        return c
+
+    return run, reps * per
+
+
+def ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_16956_b200 import api
+    from paper_2601_16956_b200 import synthetic as S
+
+    ws, rank, local = dist_info()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    rec = S.config_recipe(args.config, rank)
+    spec = rec.ranks[0]
+    state = api.materialize_payloads(spec, local, 0)
+    raw = spec.raw_bytes
+    img_est = raw + 4096 * (len(spec.objects) + 4)
+    free, _ = torch.cuda.mem_get_info(local)
+    shadow = img_est + (256 << 20) <= free - (24 << 30)  # keep room for the GEMM load
+    pool = (img_est + (64 << 20) + (2 << 20) - 1) // (2 << 20) * (2 << 20)
+    cfg = api.EngineConfig(d2h_mode=args.mode, staging_capacity_bytes=pool, raw_chunk_bytes=64 << 20,
+                           device_staging_bytes=img_est + (1 << 20) if shadow else 8 << 30,
+                           flush_workers=min(16, os.cpu_count() or 8), write_files=False)
+    eng = api.CheckpointEngine(cfg, spec.rank_id, local)
+    echo = None
+    tdir = tempfile.mkdtemp(dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
+    launches0 = api.N.lib.ts_kernel_launch_count()
+
+    def step(it, engine, write):
+        api.mutate_update_step(state, it)
+        sess = api.CheckpointSession(os.path.join(tdir, f"ckpt_{it:06d}") if write else "", it, it, echo, 1,
+                                     writes_manifest=write)
+        t = engine.issue_checkpoint(sess, state, it)
+        t.wait_snapshot()
+        t.wait_persisted()
+        if write:
+            sess.wait_complete(600)
+        st = t.stats()
+        return st, sess
+
+    it = 0
+    for _ in range(args.warmup):
+        it += 1
+        step(it, eng, False)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    stats = []
+    l0 = api.N.lib.ts_kernel_launch_count()
+    with Clocks(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            it += 1
+            st, _ = step(it, eng, False)
+            stats.append(st)
+        e1.record()
+        torch.cuda.synchronize()
+    launches = api.N.lib.ts_kernel_launch_count() - l0
+    t_ms = e0.elapsed_time(e1)
+    if ws > 1:
+        tt = torch.tensor([t_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    bytes_step = stats[0]["total_bytes"]
+    tot = torch.tensor([float(bytes_step)], device=dev)
+    if ws > 1:
+        dist.all_reduce(tot)
+    box_bytes = float(tot.item())
+    value = box_bytes * args.steps / (t_ms / 1e3) / 1e9
+    snap_ms = [s["t_snapshot_ns"] / 1e6 for s in stats]
+    pack_ms = [s["pack_ms"] for s in stats]
+    d2h_ms = [s["d2h_ms"] for s in stats]
+    image = stats[0]["image_bytes"]
+    hbm_peak, peak_kind = peaks()
+    pack_alg = raw + image  # read every raw byte, write the image (incl. alignment gaps)
+    pack_mean = statistics.mean(pack_ms)
+    # restore (one, after the loop): files written by the e2e phase below
+    # --- e2e through the public API with files on /dev/shm -------------------
+    e2e = None
+    if args.e2e_steps > 0:
+        cfg_io = api.EngineConfig(**{**cfg.__dict__, "write_files": True})
+        eng.shutdown()
+        eng_io = api.CheckpointEngine(cfg_io, spec.rank_id, local)
+        step(it + 1, eng_io, True)  # warm the file path
+        it += 1
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.e2e_steps):
+            it += 1
+            shutil.rmtree(os.path.join(tdir, f"ckpt_{it - 2:06d}"), ignore_errors=True)
+            st, sess = step(it, eng_io, True)
+        f1.record()
+        torch.cuda.synchronize()
+        e2e_ms = f0.elapsed_time(f1)
+        if ws > 1:
+            tt = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = float(tt.item())
+        e2e = {"value": round(box_bytes * args.e2e_steps / (e2e_ms / 1e3) / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(image),
+               "what": "issue -> files + footers + MANIFEST.tlv durable on /dev/shm, via the C-ABI"}
+        # restore of the last checkpoint (H2D + scatter-unpack + FNV verify)
+        man = os.path.join(tdir, f"ckpt_{it:06d}", "MANIFEST.tlv")
+        r = api.Restorer(man)
+        rs = r.restore_rank(0, local)
+        torch.cuda.synchronize()
+        t0 = time.time()
+        r2 = api.Restorer(man)
+        r2.restore_rank(0, local, into=rs)
+        torch.cuda.synchronize()
+        restore_s = time.time() - t0
+        for o, so in zip(rs.objects, spec.objects):
+            o.pattern_space, o.pattern_offset = so.space, so.offset
+        rs.seed = spec.seed
+        bad = api.pattern_mismatches(rs, it)
+        e2e["restore_gbps"] = round(raw / restore_s / 1e9, 3)
+        e2e["restore_bit_exact"] = bad == 0
+        e2e["restore_stats"] = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in r2.last_stats.items()}
+        del rs, r, r2
+        eng_io.shutdown()
+    else:
+        eng.shutdown()
+    shutil.rmtree(tdir, ignore_errors=True)
+
+    # --- training-blocked time with a synthetic fwd/bwd load ------------------
+    blocked = None
+    if args.train_steps > 0:
+        blocked = training_phase(args, api, state, spec, cfg, local, dev, it)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        r = run_reference(args)
+        if r:
+            cpu = {"value": round(r["value"], 4), "unit": "GB/s", "cores": 5, "kind": "reference",
+                   "sample": r["sample"]}
+    clocks = clk.summary()
+    if rank == 0:
+        line = {
+            "metric": "checkpoint snapshot GB/s (per GPU / box)", "value": round(value, 3), "unit": "GB/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(t_ms / args.steps, 2), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {rec.name} rank-r shard, {len(spec.objects)} objects, "
+                                   f"{bytes_step / 1e9:.3f} GB/rank", "d2h_mode": args.mode,
+                       "device_shadow": bool(shadow), "l2": "inputs > L2 (126 MB)",
+                       "step": "update(pattern kernel) + issue + snapshot + checksums (no files)"},
+            "per_gpu_gbps": round(value / ws, 3),
+            "snapshot_ms_mean": round(statistics.mean(snap_ms), 2),
+            "snapshot_gbps_mean": round(bytes_step / (statistics.mean(snap_ms) / 1e3) / 1e9, 3),
+            "d2h_gbps": round(image / (statistics.mean(d2h_ms) / 1e3) / 1e9, 3) if min(d2h_ms) > 0 else None,
+            "d2h_frac_pcie": round(image / (statistics.mean(d2h_ms) / 1e3) / 1e9 / PCIE_D2H_MEASURED_GBPS, 3)
+            if min(d2h_ms) > 0 else None,
+            "roofline": {"kernel": "pack_kernel" if args.mode != "direct" else "copy-engine DMA",
+                         "bound": "hbm", "achieved": round(pack_alg / (pack_mean / 1e3) / 1e9, 1),
+                         "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": round(pack_alg / (pack_mean / 1e3) / 1e9 / hbm_peak, 3),
+                         "traffic": None, "alg_bytes_per_launch": int(pack_alg),
+                         "launch_ms": round(pack_mean, 3)},
+            "gpu_launches": int(launches),
+            "e2e": e2e, "blocked": blocked, "cpu_baseline": cpu, "clocks": clocks,
+        }
+        print(json.dumps(line))
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def training_phase(args, api, state, spec, cfg, local, dev, it0):
+    """fwd+bwd (bf16 GEMMs) -> pre_update_barrier -> update -> issue, with and
+    without checkpointing; reports host-blocked ms per checkpoint (issue_block +
+    barrier_block, simulator.cpp:211-212) and the step-time slowdown."""
+    import torch
+
+    run, fb_ms = gemm_load(args.fwd_bwd_ms, dev)
+    eng = api.CheckpointEngine(cfg, spec.rank_id, local)
+    comp = torch.cuda.current_stream()
+    res = {}
+    for mode in ("off", "lazy"):
+        pending = None
+        it = it0 + (100 if mode == "lazy" else 0)
+        times, blocked = [], []
+        for k in range(args.train_steps + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            run()                                    # forward + backward
+            b = eng.pre_update_barrier(pending, stream=comp, host_block=1) if pending else 0
+            it += 1
+            api.mutate_update_step(state, it, stream=comp)  # optimizer update
+            ib = 0
+            if mode == "lazy":
+                sess = api.CheckpointSession("", it, it, None, 1, writes_manifest=False)
+                tt = time.perf_counter()
+                pending = eng.issue_checkpoint(sess, state, it, producer_stream=comp)
+                ib = time.perf_counter() - tt
+            torch.cuda.synchronize()
+            if k > 0:
+                times.append(time.perf_counter() - t0)
+                blocked.append(1e3 * (b / 1e9 + ib))
+        if pending:
+            pending.wait_persisted()
+        res[mode] = (statistics.mean(times), statistics.mean(blocked))
+    eng.shutdown()
+    off, lazy = res["off"][0], res["lazy"][0]
+    return {"fwd_bwd_ms": round(fb_ms, 1), "steps": args.train_steps,
+            "step_ms_no_ckpt": round(1e3 * off, 2), "step_ms_lazy_ckpt": round(1e3 * lazy, 2),
+            "slowdown_pct": round(100 * (lazy - off) / off, 2),
+            "blocked_ms_per_ckpt": round(res["lazy"][1], 3)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--mode", default="ring", choices=["ring", "direct", "zerocopy"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--train-steps", type=int, default=3)
+    ap.add_argument("--fwd-bwd-ms", type=float, default=1800.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        ours(args)
+
+
+if __name__ == "__main__":
+    main()

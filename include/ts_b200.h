@@ -1,0 +1,313 @@
+/*
+ * ts_b200.h — C-ABI of the B200-native snapshot engine (libts_b200.so).
+ *
+ * Drop-in boundary for the reference's State Provider / checkpoint-engine API
+ * ("tierstream", /root/reference/proj; paths below are relative to it). Plain
+ * pointers and sizes only; CUDA streams are passed as `void*` (cudaStream_t).
+ * Every entry point names the reference interface it replaces.
+ *
+ * Error model: every call returns ts_status. Reference exception kinds map 1:1
+ * (ts_error / stream_error / cache_timeout_error / ticket_error / format_error
+ * kinds / tlv_error, common.hpp:21-24, provider.hpp:135-140, staging.hpp:18-21,
+ * transfer.hpp:41-44, format.hpp:50-67, tlv.hpp:70-73). The message of the last
+ * failure on the calling thread is ts_last_error(), its object id (when the
+ * reference would carry one) ts_last_error_object() (-1 when none).
+ * Failures inside engine threads are deferred to the next wait on the ticket,
+ * as in the reference (transfer.cpp:105-128).
+ */
+#ifndef TS_B200_H
+#define TS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TS_ABI_VERSION 1
+
+typedef enum ts_status {
+  TS_OK = 0,
+  TS_ERR_GENERIC = 1,        /* ts_error                         common.hpp:21 */
+  TS_ERR_STREAM = 2,         /* stream_error{object_id}          provider.hpp:135 */
+  TS_ERR_CACHE_TIMEOUT = 3,  /* cache_timeout_error              staging.hpp:18 */
+  TS_ERR_TICKET = 4,         /* ticket_error                     transfer.hpp:41 */
+  TS_ERR_TLV = 5,            /* tlv::tlv_error                   tlv.hpp:70 */
+  /* format_error kinds, format.hpp:50-58, in declaration order */
+  TS_ERR_MISSING_FILE = 10,
+  TS_ERR_INCOMPLETE_FILE = 11,
+  TS_ERR_CORRUPT_OBJECT = 12,
+  TS_ERR_CORRUPT_FOOTER = 13,
+  TS_ERR_BAD_MANIFEST = 14,
+  TS_ERR_INVALID_ENTRIES = 15,
+  TS_ERR_IO = 16,
+  /* B200 side */
+  TS_ERR_CUDA = 30,          /* CUDA runtime failure / no device: the product never falls back to CPU */
+  TS_ERR_INVALID_ARG = 31
+} ts_status;
+
+const char* ts_last_error(void);
+int64_t ts_last_error_object(void);
+int ts_abi_version(void);
+
+/* ------------------------------------------------------------------------ */
+/* Enumerations (model.hpp:19-25, engine.hpp:30)                             */
+
+enum { TS_TIER_DEVICE = 0, TS_TIER_HOST = 1, TS_TIER_PERSISTENT = 2 };
+enum { TS_KIND_RAW = 0, TS_KIND_STRUCTURED = 1 };
+enum { TS_PREC_FP16 = 0, TS_PREC_FP32 = 1, TS_PREC_OPAQUE = 2 };
+enum { TS_STRATEGY_SYNC = 0, TS_STRATEGY_TWO_PHASE = 1, TS_STRATEGY_LAZY = 2 };
+
+/* How device bytes reach the pinned host pool (B200 design choice):
+ *  RING     gather-pack kernel into a bounded HBM staging ring, copy-engine D2H per window
+ *  DIRECT   one copy-engine D2H per fragment straight from the state tensors
+ *  ZEROCOPY gather-pack kernel storing straight into mapped pinned host memory
+ *  HYBRID   DIRECT for fragments >= hybrid_direct_min_bytes, RING for the rest */
+enum { TS_D2H_RING = 0, TS_D2H_DIRECT = 1, TS_D2H_ZEROCOPY = 2, TS_D2H_HYBRID = 3 };
+
+/* ------------------------------------------------------------------------ */
+/* TLV values (tlv.hpp:24-83). Handles own their children once attached.     */
+
+typedef struct ts_value ts_value;
+enum { TS_V_NULL = 0, TS_V_INT = 1, TS_V_FLOAT = 2, TS_V_STRING = 3, TS_V_BYTES = 4,
+       TS_V_LIST = 5, TS_V_MAP = 6 };
+
+ts_value* ts_value_null(void);
+ts_value* ts_value_int(int64_t v);
+ts_value* ts_value_float(double v);
+ts_value* ts_value_string(const char* s, size_t n);
+ts_value* ts_value_bytes(const void* p, size_t n);
+ts_value* ts_value_list(void);
+ts_value* ts_value_map(void);
+ts_status ts_value_list_append(ts_value* list, ts_value* item);                 /* takes item */
+ts_status ts_value_map_set(ts_value* map, const char* k, size_t kn, ts_value* v); /* takes v */
+void ts_value_free(ts_value* v);
+int ts_value_type(const ts_value* v);
+int64_t ts_value_as_int(const ts_value* v);
+double ts_value_as_float(const ts_value* v);
+/* string/bytes payload view (valid while v lives) */
+const uint8_t* ts_value_data(const ts_value* v, size_t* n);
+size_t ts_value_len(const ts_value* v); /* list/map element count */
+const ts_value* ts_value_list_get(const ts_value* v, size_t i);
+const ts_value* ts_value_map_key(const ts_value* v, size_t i, size_t* kn, const char** k);
+/* tlv::encode (tlv.cpp:191-196); *len receives the size even when cap is too small */
+ts_status ts_value_encode(const ts_value* v, uint8_t* buf, size_t cap, size_t* len);
+size_t ts_value_encoded_size(const ts_value* v);
+/* tlv::decode (tlv.cpp:198-203): strict */
+ts_status ts_value_decode(const uint8_t* buf, size_t n, ts_value** out);
+/* make_metadata_value (model.cpp:206-231) */
+ts_value* ts_make_metadata_value(int rank_id, int tp_idx, int pp_idx, int dp_idx, uint64_t seed,
+                                 uint64_t metadata_bytes, uint64_t iteration);
+
+/* ------------------------------------------------------------------------ */
+/* State descriptors (state_object / rank_state, model.hpp:34-73)            */
+
+typedef struct ts_object_desc {
+  uint64_t object_id;
+  uint8_t kind;      /* TS_KIND_* */
+  uint8_t tier;      /* TS_TIER_*: device => `data` is a device pointer */
+  uint8_t precision; /* TS_PREC_* (bookkeeping only) */
+  uint8_t _pad;
+  uint32_t file_id;
+  uint64_t size_bytes;   /* raw: payload size; structured: ignored (learned at serialization) */
+  const void* data;      /* raw payload (device or host pointer per tier) */
+  const ts_value* value; /* structured payload; must outlive the snapshot */
+} ts_object_desc;
+
+typedef struct ts_rank_info {
+  int32_t rank_id, tp_idx, pp_idx, dp_idx;
+} ts_rank_info;
+
+/* ------------------------------------------------------------------------ */
+/* Layout planner (provider.cpp:17-72). Exposed for tests and restore tools.  */
+
+typedef struct ts_fixed_assignment {
+  uint64_t object_id, file_offset, length;
+} ts_fixed_assignment;
+
+/* plan_layout: per file id (ascending) writes tensor_region_end and the fixed
+ * assignments in plan order. files_out/ends_out have room for n entries,
+ * fixed_out for n entries. Returns counts in *n_files / *n_fixed and the
+ * plan_hash (provider.cpp:17-35) in *hash. */
+ts_status ts_plan_layout(const ts_object_desc* objs, size_t n, uint64_t alignment,
+                         uint32_t* files_out, uint64_t* ends_out, size_t* n_files,
+                         ts_fixed_assignment* fixed_out, uint32_t* fixed_file_out,
+                         size_t* n_fixed, uint64_t* hash);
+
+/* FNV-1a-64 (common.hpp:44-51) on host memory. */
+uint64_t ts_fnv1a64(const void* p, size_t n, uint64_t state);
+
+/* ------------------------------------------------------------------------ */
+/* Engine (checkpoint_engine, engine.hpp:92-153)                             */
+
+typedef struct ts_engine ts_engine;
+typedef struct ts_session ts_session;
+typedef struct ts_ticket ts_ticket;
+
+typedef struct ts_engine_config {
+  /* reference knobs, engine.hpp:34-52 */
+  int32_t strategy;                 /* TS_STRATEGY_*, default lazy */
+  int32_t lazy_serialize_overlap;   /* default 1 */
+  uint64_t staging_capacity_bytes;  /* pinned host pool, allocated once (staging.hpp:23-31) */
+  int32_t flush_workers;            /* host worker threads (flush + serialize + checksum) */
+  int32_t _pad0;
+  uint64_t raw_chunk_bytes;         /* D2H window, default 16 MiB (provider.hpp:24) */
+  uint64_t serialized_chunk_bytes;  /* append chunk, default 1 MiB (provider.hpp:25) */
+  uint64_t alignment;               /* default 4096 (provider.hpp:23) */
+  int64_t cache_acquire_timeout_ns; /* < 0: wait forever; default 300 s (engine.hpp:50) */
+  int32_t overwrite;                /* default 1 */
+  /* B200 knobs */
+  int32_t d2h_mode;                 /* TS_D2H_*, default RING */
+  uint64_t device_staging_bytes;    /* HBM staging ring; >= image bytes => full device shadow */
+  uint64_t hybrid_direct_min_bytes; /* HYBRID threshold */
+  int32_t pack_ctas;                /* 0 = auto (one per SM) */
+  int32_t pack_threads;             /* threads per pack CTA, default 512 */
+  int32_t low_priority_stream;      /* snapshot streams at the lowest priority, default 1 */
+  int32_t write_files;              /* 0 = snapshot-only run (no file I/O, bench only) */
+} ts_engine_config;
+
+void ts_engine_config_default(ts_engine_config* cfg);
+
+/* checkpoint_engine ctor (engine.cpp:164-204): spawns the copier + worker pool,
+ * allocates the pinned pool and binds `device`. */
+ts_status ts_engine_create(const ts_engine_config* cfg, int rank_id, int device, ts_engine** out);
+/* checkpoint_engine::shutdown (engine.cpp:213-234) + dtor */
+ts_status ts_engine_destroy(ts_engine* e);
+
+/* Manifest echo of a layout-based session (engine.cpp:35-54); NULL => defaults of
+ * the n_ranks ctor (engine.cpp:56-66). */
+typedef struct ts_manifest_echo {
+  int32_t tp, pp, dp, zero1;
+  uint64_t seed, n_params;
+  int32_t layers, _pad;
+  uint64_t metadata_bytes;
+} ts_manifest_echo;
+
+/* checkpoint_session (engine.hpp:57-90). `writes_manifest` = 1 on the process that
+ * commits MANIFEST.tlv once all n_ranks ranks persisted (local or remote). */
+ts_status ts_session_create(const char* dir, uint64_t checkpoint_id, uint64_t iteration,
+                            const ts_manifest_echo* echo, int n_ranks, int writes_manifest,
+                            ts_session** out);
+ts_status ts_session_destroy(ts_session* s);
+/* Multi-process: per-rank manifest info blob (TLV of manifest_rank_info, format.cpp:310-335)
+ * produced locally and fed to the committing process (the NCCL allgather payload). */
+ts_status ts_session_rank_blob(ts_session* s, int rank_id, uint8_t* buf, size_t cap, size_t* len);
+ts_status ts_session_add_remote_rank(ts_session* s, const uint8_t* blob, size_t len);
+/* Register a rank's manifest info without issuing (engine.cpp:539-558 part of
+ * issue_checkpoint) and mark a rank persisted: lets a host-side coordinator
+ * assemble a manifest for ranks checkpointed elsewhere. */
+ts_status ts_session_register_rank(ts_session* s, const ts_rank_info* rank,
+                                   const ts_object_desc* objs, size_t n);
+ts_status ts_session_rank_persisted(ts_session* s, int rank_id);
+ts_status ts_session_wait_complete(ts_session* s, int64_t timeout_ns);
+int ts_session_complete(ts_session* s);
+
+/* issue_checkpoint (engine.cpp:518-619). `producer_stream` is the stream whose
+ * prior work produced the state; capture is ordered after it without blocking
+ * the host. */
+ts_status ts_issue(ts_engine* e, ts_session* s, const ts_rank_info* rank,
+                   const ts_object_desc* objs, size_t n, uint64_t iteration,
+                   void* producer_stream, ts_ticket** out);
+
+/* pre_update_barrier (engine.cpp:621-630). host_block=1: reference semantics
+ * (host waits until the state may be mutated); host_block=0: the barrier is a
+ * cudaStreamWaitEvent on `optimizer_stream` (no host block). */
+ts_status ts_pre_update_barrier(ts_engine* e, ts_ticket* t, void* optimizer_stream,
+                                int host_block, int64_t* blocked_ns);
+
+/* transfer_ticket (transfer.hpp:52-88) */
+ts_status ts_ticket_wait_captured(ts_ticket* t, int64_t* blocked_ns); /* state may be mutated */
+ts_status ts_ticket_wait_snapshot(ts_ticket* t, int64_t* blocked_ns); /* all bytes in host memory */
+ts_status ts_ticket_wait_persisted(ts_ticket* t, int64_t* blocked_ns);
+typedef struct ts_ticket_stats {
+  uint64_t checkpoint_id;
+  uint64_t total_bytes, raw_bytes, serialized_bytes, image_bytes;
+  int64_t issue_block_ns, barrier_block_ns;
+  int64_t t_captured_ns, t_snapshot_ns, t_persisted_ns; /* relative to issue start; -1 pending */
+  float pack_ms;   /* CUDA-event time of the pack kernels (RING/ZEROCOPY/HYBRID) */
+  float d2h_ms;    /* CUDA-event time from first to last D2H window */
+  uint32_t kernel_launches, copies;
+  int32_t snapshot_done, persisted_done, failed;
+} ts_ticket_stats;
+ts_status ts_ticket_stats_get(ts_ticket* t, ts_ticket_stats* out);
+/* Per-object checksum accumulated at staging (transfer.cpp:163-166) */
+ts_status ts_ticket_object_checksum(ts_ticket* t, uint64_t object_id, uint64_t* out);
+void ts_ticket_release(ts_ticket* t);
+
+/* ------------------------------------------------------------------------ */
+/* Restore (format.cpp:201-494)                                              */
+
+typedef struct ts_restore ts_restore;
+typedef struct ts_restore_object {
+  uint64_t object_id;
+  uint8_t kind, tier, precision, _pad;
+  uint32_t file_id;
+  uint64_t size_bytes;
+} ts_restore_object;
+
+/* read_manifest (format.cpp:407-428) */
+ts_status ts_restore_open(const char* manifest_path, ts_restore** out);
+void ts_restore_close(ts_restore* r);
+int ts_restore_n_ranks(ts_restore* r);
+ts_status ts_restore_rank_info(ts_restore* r, int index, ts_rank_info* out);
+/* Reads the footers of the rank's files and lists its objects in manifest order,
+ * with sizes (format.cpp:247-287 without the payload). */
+ts_status ts_restore_rank_objects(ts_restore* r, int index, ts_restore_object* out, size_t cap,
+                                  size_t* n);
+/* restore_checkpoint for one rank (format.cpp:430-494), B200 path: files -> pinned
+ * -> FNV verify -> H2D -> scatter-unpack into `dst[i].data` (device pointers of
+ * raw objects, sizes must match). Structured objects become ts_value handles
+ * fetched with ts_restore_structured. */
+typedef struct ts_restore_stats {
+  uint64_t bytes;
+  double read_s, verify_s, h2d_unpack_s, total_s;
+  float unpack_ms, h2d_ms;
+  uint32_t kernel_launches;
+} ts_restore_stats;
+ts_status ts_restore_rank(ts_restore* r, int index, const ts_object_desc* dst, size_t n,
+                          int device, void* stream, ts_restore_stats* stats);
+ts_status ts_restore_structured(ts_restore* r, int index, uint64_t object_id, ts_value** out);
+
+/* verify_checkpoint (format.cpp:496-529): never fails on a damaged checkpoint;
+ * issues are reported as (status kind, object id or -1). */
+typedef struct ts_verify_issue { int32_t kind; int32_t _pad; int64_t object_id; } ts_verify_issue;
+typedef struct ts_verify_report {
+  int32_t ok;
+  int32_t n_issues;
+  uint64_t files_checked, objects_checked;
+} ts_verify_report;
+ts_status ts_verify(const char* manifest_path, ts_verify_report* rep, ts_verify_issue* issues,
+                    size_t cap);
+
+/* ------------------------------------------------------------------------ */
+/* Device kernels of the synthetic state (pattern.hpp:57-81, model.cpp:233-244) */
+
+typedef struct ts_pattern_desc {
+  void* data;           /* device pointer */
+  uint64_t size;
+  uint64_t space;       /* pattern space (model.cpp:17-19) */
+  uint64_t offset;      /* pattern offset of byte 0 */
+} ts_pattern_desc;
+
+/* mutate_update_step on device: every fragment <- pattern(seed, space, iteration) */
+ts_status ts_pattern_fill(const ts_pattern_desc* d, size_t n, uint64_t seed, uint64_t iteration,
+                          void* stream);
+/* matches_pattern on device: *mismatched_bytes = total mismatching bytes (0 = bit-exact) */
+ts_status ts_pattern_verify(const ts_pattern_desc* d, size_t n, uint64_t seed,
+                            uint64_t iteration, void* stream, uint64_t* mismatched_bytes);
+
+/* Raw kernel entry for microbenchmarks: gather `n` device fragments into `dst`
+ * (device or mapped-host) at dst_offsets, zero-filling the gaps up to `dst_len`. */
+ts_status ts_pack(const void* const* srcs, const uint64_t* sizes, const uint64_t* dst_offsets,
+                  size_t n, void* dst, uint64_t dst_len, int ctas, int threads, void* stream);
+ts_status ts_unpack(const void* src, const uint64_t* src_offsets, void* const* dsts,
+                    const uint64_t* sizes, size_t n, int ctas, int threads, void* stream);
+
+/* Number of this library's kernels launched so far (process-wide). */
+uint64_t ts_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TS_B200_H */

@@ -1,0 +1,1117 @@
+// B200 snapshot engine (see engine.hpp for the reference mapping).
+#include "engine.hpp"
+
+#include <sys/stat.h>
+
+#include <algorithm>
+#include <cerrno>
+#include <chrono>
+#include <unordered_set>
+
+namespace tsb {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(TS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+void mkdirs(const std::string& path) {
+  std::string cur;
+  for (size_t i = 0; i <= path.size(); ++i) {
+    if (i == path.size() || path[i] == '/') {
+      if (!cur.empty() && ::mkdir(cur.c_str(), 0755) != 0 && errno != EEXIST)
+        fail(TS_ERR_IO, "cannot create directory " + cur + ": " + std::strerror(errno));
+    }
+    if (i < path.size()) cur += path[i];
+  }
+}
+std::chrono::steady_clock::time_point to_tp(int64_t ns) {
+  return std::chrono::steady_clock::time_point(std::chrono::nanoseconds(ns));
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// thread pool
+
+thread_pool::thread_pool(int n) {
+  for (int i = 0; i < std::max(1, n); ++i)
+    threads_.emplace_back([this] {
+      for (;;) {
+        std::function<void()> f;
+        {
+          std::unique_lock<std::mutex> g(mu_);
+          cv_.wait(g, [&] { return stop_ || !q_.empty(); });
+          if (q_.empty()) return;
+          f = std::move(q_.front());
+          q_.pop_front();
+        }
+        f();
+      }
+    });
+}
+
+thread_pool::~thread_pool() {
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    stop_ = true;
+  }
+  cv_.notify_all();
+  for (auto& t : threads_) t.join();
+}
+
+void thread_pool::submit(std::function<void()> f) {
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    q_.push_back(std::move(f));
+  }
+  cv_.notify_one();
+}
+
+// ---------------------------------------------------------------------------
+// pinned pool (staging.cpp:10-115 semantics over cudaHostAlloc memory)
+
+pinned_pool::pinned_pool(uint64_t capacity) : capacity_(capacity) {
+  if (capacity == 0) fail(TS_ERR_GENERIC, "staging cache: zero capacity");
+  void* p = nullptr;
+  cuda_check(cudaHostAlloc(&p, capacity, cudaHostAllocPortable | cudaHostAllocMapped),
+             "cudaHostAlloc(staging pool)");
+  base_ = static_cast<uint8_t*>(p);
+}
+
+pinned_pool::~pinned_pool() {
+  if (base_) cudaFreeHost(base_);
+}
+
+bool pinned_pool::find_locked(uint64_t size, uint64_t* off) const {
+  auto free_at = [&](uint64_t start) {
+    if (start + size > capacity_) return false;
+    auto it = live_.lower_bound(start);
+    if (it != live_.end() && it->first < start + size) return false;
+    if (it != live_.begin()) {
+      auto prev = std::prev(it);
+      if (prev->first + prev->second > start) return false;
+    }
+    return true;
+  };
+  if (free_at(bump_)) return *off = bump_, true;
+  if (free_at(0)) return *off = 0, true;
+  uint64_t cursor = 0;
+  for (const auto& [o, l] : live_) {
+    if (o >= cursor && o - cursor >= size) return *off = cursor, true;
+    cursor = std::max(cursor, o + l);
+  }
+  if (capacity_ - cursor >= size) return *off = cursor, true;
+  return false;
+}
+
+pinned_pool::region pinned_pool::acquire(uint64_t size, int64_t deadline_ns) {
+  if (size == 0) fail(TS_ERR_GENERIC, "staging cache: zero-size acquire");
+  if (size > capacity_) fail(TS_ERR_GENERIC, "staging cache: oversized request");
+  std::unique_lock<std::mutex> g(mu_);
+  const uint64_t token = next_token_++;
+  waiters_.push_back(token);
+  for (;;) {
+    uint64_t off;
+    if (waiters_.front() == token && find_locked(size, &off)) {
+      waiters_.pop_front();
+      live_.emplace(off, size);
+      allocated_ += size;
+      peak_ = std::max(peak_, allocated_);
+      bump_ = (off + size) % capacity_;
+      cv_.notify_all();
+      return {next_id_++, off, size};
+    }
+    if (deadline_ns >= 0) {
+      if (now_ns() >= deadline_ns) {
+        waiters_.erase(std::find(waiters_.begin(), waiters_.end(), token));
+        cv_.notify_all();
+        fail(TS_ERR_CACHE_TIMEOUT, "staging cache: acquire deadline exceeded");
+      }
+      cv_.wait_until(g, to_tp(deadline_ns));
+    } else {
+      cv_.wait(g);
+    }
+  }
+}
+
+void pinned_pool::release(const region& r) {
+  std::lock_guard<std::mutex> g(mu_);
+  auto it = live_.find(r.offset);
+  if (it == live_.end()) fail(TS_ERR_GENERIC, "staging cache: release of unknown or freed region");
+  allocated_ -= it->second;
+  live_.erase(it);
+  cv_.notify_all();
+}
+
+// ---------------------------------------------------------------------------
+// ticket
+
+ticket_state::~ticket_state() {
+  cudaSetDevice(device);
+  for (cudaEvent_t e : {ev_start, ev_capture, ev_d2h_first, ev_d2h_last, ev_pack0})
+    if (e) cudaEventDestroy(e);
+}
+
+void ticket_state::fail(ts_status s, const std::string& m, int64_t oid) {
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (!failed) {
+      failed = true;
+      err_status = s;
+      err = m;
+      err_oid = oid;
+    }
+  }
+  cv.notify_all();
+}
+
+void ticket_state::throw_if_failed_locked() {
+  if (failed) throw error(TS_ERR_TICKET, err, err_oid);
+}
+
+int64_t ticket_state::wait_until(const std::function<bool()>& pred) {
+  std::unique_lock<std::mutex> g(mu);
+  const int64_t t0 = now_ns();
+  cv.wait(g, [&] { return failed || pred(); });
+  throw_if_failed_locked();
+  return now_ns() - t0;
+}
+
+// ---------------------------------------------------------------------------
+// job: everything one issued checkpoint of one rank needs.
+
+struct job {
+  struct rawo {
+    uint64_t oid = 0;
+    uint32_t f = 0;
+    uint64_t file_off = 0, size = 0, img = 0;
+    const uint8_t* src = nullptr;
+    bool device = true;
+    // checksum actor state (pieces arrive in object order)
+    uint64_t fnv = fnv_seed, hashed = 0;
+    bool busy = false;
+    struct piece {
+      const uint8_t* p;
+      uint64_t len;
+      uint32_t w;
+    };
+    std::deque<piece> q;
+  };
+  struct fstate {
+    uint32_t fid = 0;
+    uint64_t tre = header_reserved, img = 0;
+    std::unique_ptr<file_writer> w;
+    int win_pending = 0, raw_pending = 0, struct_pending = 0;
+    bool appended = true, finalizing = false, finalized = false;
+    std::vector<size_t> structs;
+    std::vector<footer_entry> appends;
+    uint64_t append_end = 0;
+  };
+  struct win {
+    uint64_t lo = 0, hi = 0;
+    pinned_pool::region r;
+    cudaEvent_t ev = nullptr;
+    int refs = 0;
+    uint32_t wp_begin = 0, wp_end = 0, fs_begin = 0, fs_end = 0, hp_begin = 0, hp_end = 0;
+  };
+  struct wpiece {
+    uint32_t obj;
+    uint64_t len, win_off;
+  };
+  struct fseg {
+    uint32_t f;
+    uint64_t file_off, len, win_off;
+  };
+  struct hpiece {
+    const uint8_t* src;
+    uint64_t len, win_off;
+  };
+  struct sobj {
+    uint64_t oid = 0;
+    uint32_t f = 0;
+    const value* v = nullptr;
+    std::vector<uint8_t> enc;
+    uint64_t ck = 0;
+  };
+
+  session* sess = nullptr;
+  std::shared_ptr<ticket_state> t;
+  int rank_id = 0;
+  uint64_t iteration = 0;
+  layout_plan plan;
+  std::vector<rawo> raws;
+  std::vector<fstate> files;
+  std::vector<win> wins;
+  std::vector<wpiece> wp;
+  std::vector<fseg> fs;
+  std::vector<hpiece> hp;
+  std::vector<sobj> sobjs;
+  std::vector<dev::seg> segs;
+  std::vector<cudaEvent_t> chunk_events;  // per-job, destroyed at the end
+  uint64_t img = 0;
+  bool io = true;
+
+  std::mutex mu;
+  size_t wins_landed = 0, wins_enqueued = 0, structs_pending = 0, files_done = 0;
+  bool enqueue_done = false, snapshot_done = false, persisted = false;
+};
+
+// ---------------------------------------------------------------------------
+// engine
+
+engine::engine(const ts_engine_config& cfg, int rank_id, int device)
+    : cfg_(cfg), rank_id_(rank_id), device_(device) {
+  if (cfg_.flush_workers < 1) fail(TS_ERR_GENERIC, "engine: need at least one flush worker");
+  if (cfg_.raw_chunk_bytes == 0) fail(TS_ERR_GENERIC, "raw source: zero chunk size");
+  if (cfg_.serialized_chunk_bytes == 0) fail(TS_ERR_GENERIC, "serialize_structured: zero chunk size");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    fail(TS_ERR_CUDA, "no CUDA device: the B200 engine has no CPU fallback");
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  sms_ = dev::sm_count(device_);
+  pool_ = std::make_unique<pinned_pool>(cfg_.staging_capacity_bytes);
+  int lo_prio = 0, hi_prio = 0;
+  cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+  const int prio = cfg_.low_priority_stream ? lo_prio : hi_prio;
+  cuda_check(cudaStreamCreateWithPriority(&pack_stream_, cudaStreamNonBlocking, prio), "stream");
+  cuda_check(cudaStreamCreateWithPriority(&copy_stream_, cudaStreamNonBlocking, prio), "stream");
+  workers_ = std::make_unique<thread_pool>(cfg_.flush_workers);
+  copier_ = std::thread([this] { copier_loop(); });
+  completer_ = std::thread([this] { completer_loop(); });
+}
+
+engine::~engine() {
+  shutdown();
+  cudaSetDevice(device_);
+  if (ring_) cudaFree(ring_);
+  if (segbuf_) cudaFree(segbuf_);
+  if (pack_stream_) cudaStreamDestroy(pack_stream_);
+  if (copy_stream_) cudaStreamDestroy(copy_stream_);
+  for (auto e : ev_free_) cudaEventDestroy(e);
+}
+
+void engine::shutdown() {
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    if (stopping_ && !copier_.joinable()) return;
+    stopping_ = true;
+  }
+  cv_.notify_all();
+  if (copier_.joinable()) copier_.join();
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    copier_done_ = true;
+  }
+  cv_.notify_all();
+  if (completer_.joinable()) completer_.join();
+  // Let outstanding checksum / flush / finalize tasks run to completion.
+  if (last_job_) {
+    auto t = last_job_->t;
+    std::unique_lock<std::mutex> g(t->mu);
+    t->cv.wait(g, [&] { return t->failed || t->persisted; });
+  }
+  workers_.reset();
+  last_job_.reset();
+}
+
+cudaEvent_t engine::get_event() {
+  {
+    std::lock_guard<std::mutex> g(ev_mu_);
+    if (!ev_free_.empty()) {
+      auto e = ev_free_.back();
+      ev_free_.pop_back();
+      return e;
+    }
+  }
+  cudaEvent_t e;
+  cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync), "event");
+  return e;
+}
+
+void engine::put_event(cudaEvent_t e) {
+  std::lock_guard<std::mutex> g(ev_mu_);
+  ev_free_.push_back(e);
+}
+
+uint8_t* engine::ensure_device_ring(uint64_t bytes) {
+  if (ring_bytes_ < bytes) {
+    if (ring_) cudaFree(ring_);
+    ring_ = nullptr;
+    ring_bytes_ = 0;
+    cuda_check(cudaMalloc(&ring_, bytes), "cudaMalloc(device staging ring)");
+    ring_bytes_ = bytes;
+  }
+  return ring_;
+}
+
+void* engine::ensure_seg_buffer(uint64_t bytes) {
+  if (segbuf_bytes_ < bytes) {
+    if (segbuf_) cudaFree(segbuf_);
+    segbuf_ = nullptr;
+    cuda_check(cudaMalloc(&segbuf_, bytes), "cudaMalloc(segment table)");
+    segbuf_bytes_ = bytes;
+  }
+  return segbuf_;
+}
+
+// issue_checkpoint (engine.cpp:518-619), lazy by default.
+std::shared_ptr<ticket_state> engine::issue(session& s, const ts_rank_info& rank,
+                                            const ts_object_desc* objs, size_t n,
+                                            uint64_t iteration, cudaStream_t producer) {
+  const int64_t t0 = now_ns();
+  // One consistent device view at a time (engine.cpp:523-525).
+  if (cfg_.strategy == TS_STRATEGY_LAZY && last_job_) {
+    auto prev = last_job_->t;
+    std::unique_lock<std::mutex> g(prev->mu);
+    prev->cv.wait(g, [&] { return prev->failed || prev->snapshot; });
+    prev->throw_if_failed_locked();
+  }
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+
+  auto j = std::make_shared<job>();
+  j->sess = &s;
+  j->rank_id = rank.rank_id;
+  j->iteration = iteration;
+  j->io = cfg_.write_files != 0;
+  j->plan = plan_layout(objs, n, cfg_.alignment);
+  auto t = std::make_shared<ticket_state>();
+  j->t = t;
+  t->checkpoint_id = s.checkpoint_id();
+  t->rank_id = rank.rank_id;
+  t->device = device_;
+  t->t_issue = t0;
+  for (cudaEvent_t* e : {&t->ev_start, &t->ev_capture, &t->ev_d2h_first, &t->ev_d2h_last, &t->ev_pack0})
+    cuda_check(cudaEventCreate(e), "cudaEventCreate");
+  // The capture is ordered after everything already queued on the producer.
+  cuda_check(cudaEventRecord(t->ev_start, producer), "cudaEventRecord(producer)");
+
+  std::unordered_map<uint64_t, size_t> by_id;
+  by_id.reserve(n * 2);
+  for (size_t i = 0; i < n; ++i) by_id.emplace(objs[i].object_id, i);
+
+  // Files, image layout: each file's tensor region [4096, tre) maps to image
+  // [img, img + tre - 4096), file images 4 KiB aligned so that every object
+  // starts 16-B aligned in the image.
+  const std::string rdir = s.rank_dir(rank.rank_id);
+  if (j->io) mkdirs(rdir);
+  std::unordered_map<uint32_t, uint32_t> fidx;
+  uint64_t cursor = 0;
+  for (const auto& fp : j->plan.files) {
+    job::fstate fs;
+    fs.fid = fp.file_id;
+    fs.tre = fp.tensor_region_end;
+    cursor = align_up(cursor, 4096);
+    fs.img = cursor;
+    cursor += fp.tensor_region_end - header_reserved;
+    fs.w = std::make_unique<file_writer>(rdir + "/file_" + std::to_string(fp.file_id) + ".bin",
+                                         fp.tensor_region_end, j->plan.hash, cfg_.overwrite != 0,
+                                         j->io);
+    fs.append_end = fp.tensor_region_end;
+    fidx.emplace(fp.file_id, static_cast<uint32_t>(j->files.size()));
+    j->files.push_back(std::move(fs));
+  }
+  j->img = cursor;
+
+  // Raw objects in image order + the pack segment table covering [0, img)
+  // (zero segments for alignment gaps and inter-file padding).
+  uint64_t raw_bytes = 0, seg_end = 0;
+  auto push_seg = [&](uint64_t pos, uint64_t len, const uint8_t* src) {
+    if (len) j->segs.push_back({pos, len, src});
+    seg_end = pos + len;
+  };
+  for (size_t fi = 0; fi < j->plan.files.size(); ++fi) {
+    const auto& fp = j->plan.files[fi];
+    auto& fs = j->files[fi];
+    if (fs.img > seg_end) push_seg(seg_end, fs.img - seg_end, nullptr);
+    uint64_t foff = header_reserved;
+    for (const auto& a : fp.fixed) {
+      const ts_object_desc& d = objs[by_id.at(a.object_id)];
+      if (a.file_offset > foff)
+        push_seg(fs.img + (foff - header_reserved), a.file_offset - foff, nullptr);
+      job::rawo r;
+      r.oid = a.object_id;
+      r.f = static_cast<uint32_t>(fi);
+      r.file_off = a.file_offset;
+      r.size = a.length;
+      r.img = fs.img + (a.file_offset - header_reserved);
+      r.src = static_cast<const uint8_t*>(d.data);
+      r.device = d.tier == TS_TIER_DEVICE;
+      if (!r.src) fail(TS_ERR_INVALID_ARG, "raw object without payload", static_cast<int64_t>(r.oid));
+      push_seg(r.img, r.size, r.device ? r.src : nullptr);
+      j->raws.push_back(std::move(r));
+      fs.raw_pending += 1;
+      raw_bytes += a.length;
+      foff = a.file_offset + a.length;
+    }
+  }
+
+  // D2H windows over [0, img) and their pieces (one sweep).
+  const uint64_t W = std::min<uint64_t>(cfg_.raw_chunk_bytes, pool_->capacity());
+  {
+    size_t ri = 0, fi = 0;
+    for (uint64_t lo = 0; lo < j->img; lo += W) {
+      job::win w;
+      w.lo = lo;
+      w.hi = std::min(lo + W, j->img);
+      w.wp_begin = static_cast<uint32_t>(j->wp.size());
+      w.fs_begin = static_cast<uint32_t>(j->fs.size());
+      w.hp_begin = static_cast<uint32_t>(j->hp.size());
+      while (ri < j->raws.size() && j->raws[ri].img + j->raws[ri].size <= w.lo) ++ri;
+      for (size_t k = ri; k < j->raws.size() && j->raws[k].img < w.hi; ++k) {
+        const auto& r = j->raws[k];
+        const uint64_t a = std::max(w.lo, r.img), b = std::min(w.hi, r.img + r.size);
+        if (b <= a) continue;
+        j->wp.push_back({static_cast<uint32_t>(k), b - a, a - w.lo});
+        if (!r.device) j->hp.push_back({r.src + (a - r.img), b - a, a - w.lo});
+      }
+      while (fi < j->files.size() && j->files[fi].img + (j->files[fi].tre - header_reserved) <= w.lo) ++fi;
+      for (size_t k = fi; k < j->files.size() && j->files[k].img < w.hi; ++k) {
+        auto& f = j->files[k];
+        const uint64_t fe = f.img + (f.tre - header_reserved);
+        const uint64_t a = std::max(w.lo, f.img), b = std::min(w.hi, fe);
+        if (b <= a) continue;
+        j->fs.push_back({static_cast<uint32_t>(k), header_reserved + (a - f.img), b - a, a - w.lo});
+        if (j->io) f.win_pending += 1;
+      }
+      w.wp_end = static_cast<uint32_t>(j->wp.size());
+      w.fs_end = static_cast<uint32_t>(j->fs.size());
+      w.hp_end = static_cast<uint32_t>(j->hp.size());
+      j->wins.push_back(w);
+    }
+  }
+
+  // Structured objects, in rank.objects order (the canonical append order).
+  for (size_t i = 0; i < n; ++i) {
+    if (objs[i].kind != TS_KIND_STRUCTURED) continue;
+    if (!objs[i].value) fail(TS_ERR_INVALID_ARG, "structured object without a value", static_cast<int64_t>(objs[i].object_id));
+    job::sobj so;
+    so.oid = objs[i].object_id;
+    so.f = fidx.at(objs[i].file_id);
+    so.v = V(objs[i].value);
+    auto& fs = j->files[so.f];
+    fs.structs.push_back(j->sobjs.size());
+    fs.struct_pending += 1;
+    fs.appended = false;
+    j->sobjs.push_back(std::move(so));
+  }
+  j->structs_pending = j->sobjs.size();
+
+  s.register_rank(make_rank_info(rank, objs, n));
+
+  t->raw_bytes = raw_bytes;
+  t->image_bytes = j->img;
+  t->total_bytes = raw_bytes;  // serialized bytes added as encoded
+
+  const bool inline_ser = cfg_.strategy == TS_STRATEGY_LAZY && !cfg_.lazy_serialize_overlap;
+  if (inline_ser) {
+    for (size_t k = 0; k < j->sobjs.size(); ++k) serialize_task(j, k);
+  } else {
+    for (size_t k = 0; k < j->sobjs.size(); ++k) workers_->submit([this, j, k] { serialize_task(j, k); });
+  }
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    jobs_.push_back(j);
+  }
+  cv_.notify_all();
+  last_job_ = j;
+
+  if (cfg_.strategy == TS_STRATEGY_SYNC) {
+    t->wait_until([&] { return t->persisted; });
+  } else if (cfg_.strategy == TS_STRATEGY_TWO_PHASE) {
+    t->wait_until([&] { return t->snapshot; });
+  }
+  t->issue_block_ns = now_ns() - t0;
+  return t;
+}
+
+int64_t engine::pre_update_barrier(const std::shared_ptr<ticket_state>& t, cudaStream_t opt_stream,
+                                   int host_block) {
+  if (!t || cfg_.strategy != TS_STRATEGY_LAZY) return 0;
+  const int64_t t0 = now_ns();
+  if (host_block == 2) {  // exact reference semantics: wait_snapshot (transfer.cpp:114-120)
+    t->wait_until([&] { return t->snapshot; });
+    const int64_t dt = now_ns() - t0;
+    std::lock_guard<std::mutex> g(t->mu);
+    t->barrier_block_ns += dt;
+    return dt;
+  }
+  t->wait_until([&] { return t->capture_recorded; });
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  if (host_block) {
+    cuda_check(cudaEventSynchronize(t->ev_capture), "barrier: cudaEventSynchronize");
+  } else {
+    cuda_check(cudaStreamWaitEvent(opt_stream, t->ev_capture, 0), "barrier: cudaStreamWaitEvent");
+  }
+  const int64_t dt = now_ns() - t0;
+  std::lock_guard<std::mutex> g(t->mu);
+  if (host_block && t->t_captured < 0) t->t_captured = now_ns() - t->t_issue;
+  t->barrier_block_ns += dt;
+  return dt;
+}
+
+// --- copier: enqueues the device side of each job -------------------------
+
+void engine::copier_loop() {
+  cudaSetDevice(device_);
+  for (;;) {
+    std::shared_ptr<job> j;
+    {
+      std::unique_lock<std::mutex> g(mu_);
+      cv_.wait(g, [&] { return stopping_ || !jobs_.empty(); });
+      if (jobs_.empty()) return;
+      j = jobs_.front();
+      jobs_.pop_front();
+    }
+    try {
+      run_job(j);
+    } catch (const error& e) {
+      j->t->fail(e.status, std::string("staging failed: ") + e.what(), e.object_id);
+    } catch (const std::exception& e) {
+      j->t->fail(TS_ERR_GENERIC, std::string("staging failed: ") + e.what());
+    }
+    {
+      std::lock_guard<std::mutex> g(j->mu);
+      j->enqueue_done = true;
+    }
+    // The capture event must exist even on failure so barriers do not hang.
+    {
+      std::lock_guard<std::mutex> g(j->t->mu);
+      if (!j->t->capture_recorded) {
+        cudaEventRecord(j->t->ev_capture, pack_stream_);
+        j->t->capture_recorded = true;
+      }
+    }
+    j->t->cv.notify_all();
+    check_snapshot(j);
+    for (size_t f = 0; f < j->files.size(); ++f) file_progress(j, f);
+  }
+}
+
+void engine::run_job(const std::shared_ptr<job>& j) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  auto& t = *j->t;
+  const int mode = cfg_.d2h_mode == TS_D2H_HYBRID ? TS_D2H_RING : cfg_.d2h_mode;
+  const int64_t timeout = cfg_.cache_acquire_timeout_ns;
+  const int ctas = cfg_.pack_ctas > 0 ? cfg_.pack_ctas : sms_ * 2;
+  const int threads = cfg_.pack_threads > 0 ? cfg_.pack_threads : 512;
+  auto mark_capture = [&](cudaStream_t st) {
+    cuda_check(cudaEventRecord(t.ev_capture, st), "cudaEventRecord(capture)");
+    {
+      std::lock_guard<std::mutex> g(t.mu);
+      t.capture_recorded = true;
+    }
+    t.cv.notify_all();
+  };
+  auto push_window = [&](size_t w) {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      inflight_.push_back({j, w});
+    }
+    cv_.notify_all();
+    std::lock_guard<std::mutex> g(j->mu);
+    j->wins_enqueued += 1;
+  };
+  auto acquire = [&](job::win& w) {
+    w.r = pool_->acquire(w.hi - w.lo, timeout >= 0 ? now_ns() + timeout : -1);
+    w.ev = get_event();
+  };
+  auto failed = [&] {
+    std::lock_guard<std::mutex> g(t.mu);
+    return t.failed;
+  };
+
+  dev::seg* d_segs = nullptr;
+  if (j->img > 0 && mode != TS_D2H_DIRECT) {
+    d_segs = static_cast<dev::seg*>(ensure_seg_buffer(j->segs.size() * sizeof(dev::seg)));
+    // Upload before waiting on the producer (a pageable H2D syncs its stream).
+    cuda_check(cudaMemcpyAsync(d_segs, j->segs.data(), j->segs.size() * sizeof(dev::seg),
+                               cudaMemcpyHostToDevice, pack_stream_), "upload segment table");
+  }
+  cuda_check(cudaStreamWaitEvent(pack_stream_, t.ev_start, 0), "wait producer");
+  cuda_check(cudaStreamWaitEvent(copy_stream_, t.ev_start, 0), "wait producer");
+  cuda_check(cudaEventRecord(t.ev_pack0, mode == TS_D2H_DIRECT ? copy_stream_ : pack_stream_), "event");
+  if (j->img == 0) {
+    mark_capture(pack_stream_);
+    return;
+  }
+  const uint32_t nsegs = static_cast<uint32_t>(j->segs.size());
+  const uint64_t W = j->wins.front().hi - j->wins.front().lo;
+
+  if (mode == TS_D2H_RING) {
+    // HBM staging: whole image when it fits (device shadow), else two slots of
+    // whole windows, packs running ahead of the copies.
+    const uint64_t want = align_up(j->img, 256);
+    const uint64_t cap = std::max<uint64_t>(cfg_.device_staging_bytes, 2 * W);
+    uint64_t chunk;
+    int nslots;
+    if (cap >= want) {
+      chunk = want;
+      nslots = 1;
+    } else {
+      chunk = std::max<uint64_t>(W, (cap / 2) / W * W);
+      nslots = 2;
+    }
+    uint8_t* ring = ensure_device_ring(nslots == 1 ? want : 2 * chunk);
+    const size_t nchunks = (j->img + chunk - 1) / chunk;
+    j->chunk_events.assign(nchunks, nullptr);
+    size_t w = 0;
+    cuda_check(cudaEventRecord(t.ev_d2h_first, copy_stream_), "event");
+    for (size_t c = 0; c < nchunks && !failed(); ++c) {
+      const uint64_t clo = c * chunk, chi = std::min(j->img, clo + chunk);
+      uint8_t* slot = ring + (nslots == 1 ? 0 : (c % 2) * chunk);
+      if (c >= 2) cuda_check(cudaStreamWaitEvent(pack_stream_, j->chunk_events[c - 2], 0), "slot wait");
+      dev::launch_pack(d_segs, nsegs, clo, chi, slot, ctas, threads, pack_stream_);
+      t.kernel_launches += 1;
+      cuda_check(cudaGetLastError(), "pack kernel launch");
+      cudaEvent_t packed;
+      cuda_check(cudaEventCreateWithFlags(&packed, cudaEventDisableTiming), "event");
+      cuda_check(cudaEventRecord(packed, pack_stream_), "event");
+      if (c + 1 == nchunks) mark_capture(pack_stream_);
+      cuda_check(cudaStreamWaitEvent(copy_stream_, packed, 0), "wait pack");
+      cudaEventDestroy(packed);  // destruction is deferred until the event completes
+      for (; w < j->wins.size() && j->wins[w].lo < chi; ++w) {
+        auto& win = j->wins[w];
+        acquire(win);
+        cuda_check(cudaMemcpyAsync(pool_->data(win.r), slot + (win.lo - clo), win.hi - win.lo,
+                                   cudaMemcpyDeviceToHost, copy_stream_), "D2H window");
+        t.copies += 1;
+        cuda_check(cudaEventRecord(win.ev, copy_stream_), "event");
+        push_window(w);
+        if (failed()) break;
+      }
+      cudaEvent_t done;
+      cuda_check(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "event");
+      cuda_check(cudaEventRecord(done, copy_stream_), "event");
+      j->chunk_events[c] = done;
+    }
+    cuda_check(cudaEventRecord(t.ev_d2h_last, copy_stream_), "event");
+  } else if (mode == TS_D2H_ZEROCOPY) {
+    uint8_t* dbase = nullptr;
+    cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dbase), pool_->base(), 0),
+               "cudaHostGetDevicePointer");
+    cuda_check(cudaEventRecord(t.ev_d2h_first, pack_stream_), "event");
+    for (size_t w = 0; w < j->wins.size() && !failed(); ++w) {
+      auto& win = j->wins[w];
+      acquire(win);
+      dev::launch_pack(d_segs, nsegs, win.lo, win.hi, dbase + win.r.offset, ctas, threads, pack_stream_);
+      t.kernel_launches += 1;
+      cuda_check(cudaGetLastError(), "pack kernel launch");
+      cuda_check(cudaEventRecord(win.ev, pack_stream_), "event");
+      push_window(w);
+    }
+    cuda_check(cudaEventRecord(t.ev_d2h_last, pack_stream_), "event");
+    mark_capture(pack_stream_);
+  } else {  // DIRECT: copy-engine DMA per fragment piece, gaps zeroed on the host
+    cuda_check(cudaEventRecord(t.ev_d2h_first, copy_stream_), "event");
+    size_t k = 0;
+    for (size_t w = 0; w < j->wins.size() && !failed(); ++w) {
+      auto& win = j->wins[w];
+      acquire(win);
+      uint8_t* dst = pool_->data(win.r);
+      while (k < j->segs.size() && j->segs[k].pos + j->segs[k].len <= win.lo) ++k;
+      for (size_t q = k; q < j->segs.size() && j->segs[q].pos < win.hi; ++q) {
+        const auto& sg = j->segs[q];
+        const uint64_t a = std::max(win.lo, sg.pos), b = std::min(win.hi, sg.pos + sg.len);
+        if (b <= a) continue;
+        if (sg.src) {
+          cuda_check(cudaMemcpyAsync(dst + (a - win.lo), sg.src + (a - sg.pos), b - a,
+                                     cudaMemcpyDeviceToHost, copy_stream_), "D2H fragment");
+          t.copies += 1;
+        } else {
+          std::memset(dst + (a - win.lo), 0, b - a);
+        }
+      }
+      cuda_check(cudaEventRecord(win.ev, copy_stream_), "event");
+      push_window(w);
+    }
+    cuda_check(cudaEventRecord(t.ev_d2h_last, copy_stream_), "event");
+    mark_capture(copy_stream_);
+  }
+}
+
+// --- completer: observes window completions in order ----------------------
+
+void engine::completer_loop() {
+  cudaSetDevice(device_);
+  for (;;) {
+    pending_window pw;
+    {
+      std::unique_lock<std::mutex> g(mu_);
+      cv_.wait(g, [&] { return !inflight_.empty() || copier_done_; });
+      if (inflight_.empty()) return;
+      pw = inflight_.front();
+      inflight_.pop_front();
+    }
+    auto& j = pw.j;
+    auto& win = j->wins[pw.w];
+    const cudaError_t e = cudaEventSynchronize(win.ev);
+    put_event(win.ev);
+    win.ev = nullptr;
+    if (e != cudaSuccess) {
+      j->t->fail(TS_ERR_CUDA, std::string("staging failed: ") + cudaGetErrorString(e));
+      {
+        std::lock_guard<std::mutex> g(j->mu);
+        j->wins_landed += 1;
+      }
+      pool_->release(win.r);
+      continue;
+    }
+    {
+      std::lock_guard<std::mutex> g(j->t->mu);
+      if (j->t->t_captured < 0 && j->t->capture_recorded && cudaEventQuery(j->t->ev_capture) == cudaSuccess)
+        j->t->t_captured = now_ns() - j->t->t_issue;
+    }
+    window_landed(j, pw.w);
+  }
+}
+
+void engine::window_landed(const std::shared_ptr<job>& j, size_t wi) {
+  auto& w = j->wins[wi];
+  uint8_t* base = pool_->data(w.r);
+  for (uint32_t k = w.hp_begin; k < w.hp_end; ++k)
+    std::memcpy(base + j->hp[k].win_off, j->hp[k].src, j->hp[k].len);  // host-tier bytes
+  std::vector<uint32_t> sched;
+  bool release_now = false;
+  {
+    std::lock_guard<std::mutex> g(j->mu);
+    w.refs = static_cast<int>(w.wp_end - w.wp_begin) + ((j->io && w.fs_end > w.fs_begin) ? 1 : 0);
+    for (uint32_t k = w.wp_begin; k < w.wp_end; ++k) {
+      auto& r = j->raws[j->wp[k].obj];
+      r.q.push_back({base + j->wp[k].win_off, j->wp[k].len, static_cast<uint32_t>(wi)});
+      if (!r.busy) {
+        r.busy = true;
+        sched.push_back(j->wp[k].obj);
+      }
+    }
+    j->wins_landed += 1;
+    release_now = w.refs == 0;
+  }
+  if (release_now) pool_->release(w.r);
+  for (uint32_t o : sched) workers_->submit([this, j, o] { hash_task(j, o); });
+  if (j->io && w.fs_end > w.fs_begin) workers_->submit([this, j, wi] { flush_window(j, wi); });
+  check_snapshot(j);
+}
+
+void engine::window_release_ref(const std::shared_ptr<job>& j, size_t wi) {
+  bool rel;
+  {
+    std::lock_guard<std::mutex> g(j->mu);
+    rel = --j->wins[wi].refs == 0;
+  }
+  if (rel) pool_->release(j->wins[wi].r);
+}
+
+// Object checksum actor: consumes landed pieces of one raw object in order
+// (transfer.cpp:71-83 without the global monitor; objects hash in parallel).
+void engine::hash_task(const std::shared_ptr<job>& j, size_t oi) {
+  auto& r = j->raws[oi];
+  for (;;) {
+    job::rawo::piece p;
+    {
+      std::lock_guard<std::mutex> g(j->mu);
+      if (r.q.empty()) {
+        r.busy = false;
+        return;
+      }
+      p = r.q.front();
+      r.q.pop_front();
+    }
+    r.fnv = fnv1a64(p.p, p.len, r.fnv);
+    bool done;
+    {
+      std::lock_guard<std::mutex> g(j->mu);
+      r.hashed += p.len;
+      done = r.hashed == r.size;
+      if (done) j->files[r.f].raw_pending -= 1;
+    }
+    if (done) {
+      std::lock_guard<std::mutex> g(j->t->mu);
+      j->t->checksums[r.oid] = r.fnv;
+    }
+    window_release_ref(j, p.w);
+    if (done) file_progress(j, r.f);
+  }
+}
+
+void engine::flush_window(const std::shared_ptr<job>& j, size_t wi) {
+  auto& w = j->wins[wi];
+  const uint8_t* base = pool_->data(w.r);
+  bool ok = true;
+  {
+    std::lock_guard<std::mutex> g(j->t->mu);
+    ok = !j->t->failed;
+  }
+  if (ok) {
+    try {
+      for (uint32_t k = w.fs_begin; k < w.fs_end; ++k) {
+        const auto& s = j->fs[k];
+        j->files[s.f].w->write_at(s.file_off, base + s.win_off, s.len);
+      }
+    } catch (const error& e) {
+      j->t->fail(e.status, std::string("flush failed: ") + e.what(), e.object_id);
+    }
+  }
+  {
+    std::lock_guard<std::mutex> g(j->mu);
+    for (uint32_t k = w.fs_begin; k < w.fs_end; ++k) j->files[j->fs[k].f].win_pending -= 1;
+  }
+  window_release_ref(j, wi);
+  for (uint32_t k = w.fs_begin; k < w.fs_end; ++k) file_progress(j, j->fs[k].f);
+}
+
+// run_serializer (engine.cpp:341-386): encode on a worker; once every structured
+// object of a file is encoded, lay the append region out in rank.objects order,
+// split in serialized_chunk_bytes entries (the canonical single-flusher bytes).
+void engine::serialize_task(const std::shared_ptr<job>& j, size_t si) {
+  auto& so = j->sobjs[si];
+  try {
+    so.enc = encode(*so.v);
+  } catch (const error& e) {
+    j->t->fail(TS_ERR_STREAM, "object " + std::to_string(so.oid) + ": " + e.what(),
+               static_cast<int64_t>(so.oid));
+  }
+  so.ck = fnv1a64(so.enc.data(), so.enc.size());
+  bool file_ready;
+  {
+    std::lock_guard<std::mutex> g(j->mu);
+    file_ready = --j->files[so.f].struct_pending == 0;
+    j->structs_pending -= 1;
+  }
+  {
+    std::lock_guard<std::mutex> g(j->t->mu);
+    j->t->checksums[so.oid] = so.ck;
+    j->t->serialized_bytes += so.enc.size();
+    j->t->total_bytes += so.enc.size();
+  }
+  if (file_ready) {
+    auto& f = j->files[so.f];
+    const uint64_t chunk = std::min<uint64_t>(cfg_.serialized_chunk_bytes, pool_->capacity());
+    uint64_t cur = f.tre;
+    std::vector<footer_entry> entries;
+    try {
+      for (size_t k : f.structs) {
+        const auto& s = j->sobjs[k];
+        if (s.enc.empty()) continue;  // failed encode
+        f.w->write_at(cur, s.enc.data(), s.enc.size());
+        for (uint64_t b = 0; b < s.enc.size(); b += chunk) {
+          const uint64_t len = std::min<uint64_t>(chunk, s.enc.size() - b);
+          entries.push_back({s.oid, 1, cur + b, len, b, s.ck});
+        }
+        cur += s.enc.size();
+      }
+    } catch (const error& e) {
+      j->t->fail(e.status, std::string("flush failed: ") + e.what(), e.object_id);
+    }
+    {
+      std::lock_guard<std::mutex> g(j->mu);
+      f.appends = std::move(entries);
+      f.append_end = cur;
+      f.appended = true;
+    }
+  }
+  check_snapshot(j);
+  if (file_ready) file_progress(j, so.f);
+}
+
+void engine::check_snapshot(const std::shared_ptr<job>& j) {
+  bool now_done = false;
+  {
+    std::lock_guard<std::mutex> g(j->mu);
+    if (!j->snapshot_done && j->enqueue_done && j->wins_landed == j->wins_enqueued &&
+        j->structs_pending == 0) {
+      j->snapshot_done = true;
+      now_done = true;
+    }
+  }
+  if (now_done) {
+    {
+      std::lock_guard<std::mutex> g(j->t->mu);
+      if (!j->t->failed && j->wins_landed == j->wins.size()) {
+        j->t->snapshot = true;
+        j->t->t_snapshot = now_ns() - j->t->t_issue;
+        cudaEventElapsedTime(&j->t->d2h_ms, j->t->ev_d2h_first, j->t->ev_d2h_last);
+        cudaEventElapsedTime(&j->t->pack_ms, j->t->ev_pack0, j->t->ev_capture);
+        if (j->t->t_captured < 0) j->t->t_captured = j->t->t_snapshot;
+      }
+    }
+    j->t->cv.notify_all();
+  }
+}
+
+void engine::file_progress(const std::shared_ptr<job>& j, size_t fi) {
+  auto& f = j->files[fi];
+  {
+    std::lock_guard<std::mutex> g(j->mu);
+    if (f.finalizing || !j->enqueue_done || f.win_pending != 0 || f.raw_pending != 0 || !f.appended)
+      return;
+    if (j->wins_landed != j->wins.size()) return;
+    f.finalizing = true;
+  }
+  {
+    std::lock_guard<std::mutex> g(j->t->mu);
+    if (j->t->failed) return;
+  }
+  // finalize_file_locked (engine.cpp:470-514): raw entries from the plan, then
+  // appends, sorted by file offset.
+  std::vector<footer_entry> entries;
+  const auto& fp = j->plan.files[fi];
+  entries.reserve(fp.fixed.size() + f.appends.size());
+  {
+    std::lock_guard<std::mutex> g(j->t->mu);
+    for (const auto& a : fp.fixed)
+      entries.push_back({a.object_id, 0, a.file_offset, a.length, 0, j->t->checksums.at(a.object_id)});
+  }
+  entries.insert(entries.end(), f.appends.begin(), f.appends.end());
+  std::sort(entries.begin(), entries.end(),
+            [](const footer_entry& a, const footer_entry& b) { return a.file_offset < b.file_offset; });
+  try {
+    f.w->finalize_at(f.append_end, entries);
+  } catch (const error& e) {
+    j->t->fail(e.status, std::string("finalize failed: ") + e.what(), e.object_id);
+    return;
+  }
+  f.w.reset();  // close the descriptor
+  bool all = false;
+  {
+    std::lock_guard<std::mutex> g(j->mu);
+    f.finalized = true;
+    all = ++j->files_done == j->files.size() && !j->persisted;
+    if (all) j->persisted = true;
+  }
+  if (!all) return;
+  {
+    std::lock_guard<std::mutex> g(j->t->mu);
+    j->t->persisted = true;
+    j->t->t_persisted = now_ns() - j->t->t_issue;
+  }
+  for (auto e : j->chunk_events)
+    if (e) cudaEventDestroy(e);
+  j->chunk_events.clear();
+  try {
+    j->sess->rank_persisted(j->rank_id);
+  } catch (const error& e) {
+    j->t->fail(e.status, std::string("manifest failed: ") + e.what());
+  }
+  j->t->cv.notify_all();
+}
+
+// ---------------------------------------------------------------------------
+// session (engine.cpp:35-117): manifest written last, ranks sorted by id.
+
+manifest_rank make_rank_info(const ts_rank_info& rank, const ts_object_desc* objs, size_t n) {
+  manifest_rank info;
+  info.rank_id = rank.rank_id;
+  info.tp_idx = rank.tp_idx;
+  info.pp_idx = rank.pp_idx;
+  info.dp_idx = rank.dp_idx;
+  std::vector<uint32_t> fids;
+  for (size_t i = 0; i < n; ++i) fids.push_back(objs[i].file_id);
+  std::sort(fids.begin(), fids.end());
+  fids.erase(std::unique(fids.begin(), fids.end()), fids.end());
+  std::unordered_map<uint32_t, size_t> at;
+  for (uint32_t f : fids) {
+    at.emplace(f, info.files.size());
+    manifest_file mf;
+    mf.file_id = f;
+    mf.path = rank_dir_name(rank.rank_id) + "/file_" + std::to_string(f) + ".bin";
+    info.files.push_back(std::move(mf));
+  }
+  for (size_t i = 0; i < n; ++i) {
+    info.files[at.at(objs[i].file_id)].object_ids.push_back(objs[i].object_id);
+    info.objects.push_back({objs[i].object_id, objs[i].kind, objs[i].tier, objs[i].precision,
+                            objs[i].file_id});
+  }
+  return info;
+}
+
+session::session(const std::string& dir, uint64_t ckpt_id, uint64_t iteration,
+                 const ts_manifest_echo* echo, int n_ranks, bool writes)
+    : dir_(dir), n_ranks_(n_ranks), writes_(writes) {
+  m_.checkpoint_id = ckpt_id;
+  m_.iteration = iteration;
+  if (echo) {
+    m_.tp = echo->tp;
+    m_.pp = echo->pp;
+    m_.dp = echo->dp;
+    m_.zero1 = echo->zero1 != 0;
+    m_.seed = echo->seed;
+    m_.n_params = echo->n_params;
+    m_.layers = echo->layers;
+    m_.metadata_bytes = echo->metadata_bytes;
+  }
+  if (writes_ || !dir_.empty()) mkdirs(dir_);
+}
+
+void session::register_rank(manifest_rank info) {
+  std::lock_guard<std::mutex> g(mu_);
+  const int id = info.rank_id;
+  ranks_[id] = std::move(info);
+  persisted_.emplace(id, false);
+}
+
+std::vector<uint8_t> session::rank_blob(int rank_id) {
+  std::lock_guard<std::mutex> g(mu_);
+  auto it = ranks_.find(rank_id);
+  if (it == ranks_.end()) fail(TS_ERR_INVALID_ARG, "session: unknown rank");
+  return encode(rank_to_value(it->second));
+}
+
+void session::add_remote_rank(const uint8_t* blob, size_t n) {
+  manifest_rank r = rank_from_value(decode(blob, n));
+  std::unique_lock<std::mutex> g(mu_);
+  const int id = r.rank_id;
+  ranks_[id] = std::move(r);
+  persisted_[id] = true;
+  maybe_commit_locked(g);
+}
+
+void session::rank_persisted(int rank_id) {
+  std::unique_lock<std::mutex> g(mu_);
+  persisted_[rank_id] = true;
+  maybe_commit_locked(g);
+}
+
+void session::maybe_commit_locked(std::unique_lock<std::mutex>& g) {
+  int done = 0;
+  for (const auto& [id, p] : persisted_) done += p ? 1 : 0;
+  if (complete_ || committing_) return;
+  if (!writes_) {
+    if (done == static_cast<int>(persisted_.size())) {
+      complete_ = true;
+      cv_.notify_all();
+    }
+    return;
+  }
+  if (done < n_ranks_) return;
+  committing_ = true;
+  manifest m = m_;
+  m.complete = true;
+  for (const auto& [id, r] : ranks_) m.ranks.push_back(r);
+  g.unlock();
+  std::string err;
+  try {
+    write_manifest(dir_ + "/MANIFEST.tlv", m);
+  } catch (const error& e) {
+    err = e.what();
+  }
+  g.lock();
+  commit_error_ = err;
+  complete_ = true;
+  cv_.notify_all();
+  if (!err.empty()) fail(TS_ERR_IO, err);
+}
+
+bool session::wait_complete(int64_t timeout_ns) {
+  std::unique_lock<std::mutex> g(mu_);
+  if (timeout_ns < 0) cv_.wait(g, [&] { return complete_; });
+  else cv_.wait_for(g, std::chrono::nanoseconds(timeout_ns), [&] { return complete_; });
+  if (complete_ && !commit_error_.empty()) fail(TS_ERR_IO, commit_error_);
+  return complete_;
+}
+
+bool session::complete() {
+  std::lock_guard<std::mutex> g(mu_);
+  return complete_;
+}
+
+}  // namespace tsb

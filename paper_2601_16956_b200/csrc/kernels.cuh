@@ -1,0 +1,63 @@
+// Device side of the B200 snapshot engine (sm_100a).
+//
+// All kernels work on a "segment table": a list of byte ranges laid end to end
+// in a virtual space (the per-rank checkpoint image for pack/unpack, the
+// concatenated fragments for pattern fill/verify), sorted by virtual offset.
+// Work is cut in fixed-size tiles of that virtual space and handed to warps by
+// a persistent grid, so thousands of tiny fragments and a few huge ones cost the
+// same per byte (no per-fragment launches, no idle lanes on small fragments).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tsb::dev {
+
+// One piece of the image. src == nullptr => zero fill (alignment gaps).
+struct seg {
+  uint64_t pos;  // virtual (image) offset
+  uint64_t len;
+  const uint8_t* src;
+};
+
+// One destination piece of an unpack (restore): image [pos, pos+len) -> dst.
+struct useg {
+  uint64_t pos;
+  uint64_t len;
+  uint8_t* dst;
+};
+
+// One fragment of the synthetic state: virtual [pos, pos+len) <-> data,
+// whose byte 0 is byte `offset` of pattern space `space`.
+struct pseg {
+  uint64_t pos;
+  uint64_t len;
+  uint8_t* data;
+  uint64_t space;
+  uint64_t offset;
+};
+
+constexpr uint32_t kTileBytes = 32768;  // virtual bytes per warp task
+
+// Gather-pack: writes image bytes [lo, hi) into dst (dst[0] = image byte lo).
+// dst may be device memory (RING) or mapped pinned host memory (ZEROCOPY).
+void launch_pack(const seg* d_segs, uint32_t nsegs, uint64_t lo, uint64_t hi, uint8_t* dst,
+                 int ctas, int threads, cudaStream_t st);
+
+// Scatter-unpack: image bytes [lo, hi) held in src (src[0] = image byte lo)
+// to the destination pieces that intersect the range.
+void launch_unpack(const useg* d_segs, uint32_t nsegs, uint64_t lo, uint64_t hi,
+                   const uint8_t* src, int ctas, int threads, cudaStream_t st);
+
+void launch_pattern_fill(const pseg* d_segs, uint32_t nsegs, uint64_t total, uint64_t seed,
+                         uint64_t iteration, int ctas, int threads, cudaStream_t st);
+void launch_pattern_verify(const pseg* d_segs, uint32_t nsegs, uint64_t total, uint64_t seed,
+                           uint64_t iteration, unsigned long long* d_mismatch, int ctas,
+                           int threads, cudaStream_t st);
+
+int sm_count(int device);
+unsigned long long launches();
+void count_launch();
+
+}  // namespace tsb::dev

@@ -1,0 +1,459 @@
+// Restore and verify (format.cpp:201-529), B200 path:
+//   files --pread--> pinned window ring --H2D--> HBM window ring --unpack--> shards
+// with per-object FNV verification on host threads overlapping the transfers.
+#include <fcntl.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <unordered_map>
+#include <unordered_set>
+
+#include "engine.hpp"
+#include "restore.hpp"
+
+namespace tsb {
+
+namespace {
+
+struct fd_holder {
+  int fd = -1;
+  ~fd_holder() {
+    if (fd >= 0) ::close(fd);
+  }
+};
+
+// Process-wide staging reused across restores (pinning is slow; allocate once).
+std::mutex g_stage_mu;
+uint8_t* g_pinned = nullptr;
+uint64_t g_pinned_bytes = 0;
+
+uint8_t* pinned_stage(uint64_t bytes) {
+  if (g_pinned_bytes < bytes) {
+    if (g_pinned) cudaFreeHost(g_pinned);
+    g_pinned = nullptr;
+    g_pinned_bytes = 0;
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&g_pinned), bytes, cudaHostAllocPortable),
+               "cudaHostAlloc(restore ring)");
+    g_pinned_bytes = bytes;
+  }
+  return g_pinned;
+}
+
+}  // namespace
+
+void restore_handle::load_rank(int index) {
+  auto& rc = ranks.at(static_cast<size_t>(index));
+  if (rc.loaded) return;
+  const auto& r = m.ranks.at(static_cast<size_t>(index));
+  for (const auto& mf : r.files) {
+    file_info fi;
+    fi.file_id = mf.file_id;
+    fi.path = base + "/" + mf.path;
+    fi.entries = read_footer(fi.path, &fi.size);
+    fi.region_end = header_reserved;
+    for (const auto& e : fi.entries) {
+      if (e.file_offset + e.length > fi.size)
+        fail(TS_ERR_CORRUPT_FOOTER, "entry range outside the file", static_cast<int64_t>(e.object_id));
+      if (e.kind == 0) fi.region_end = std::max(fi.region_end, e.file_offset + e.length);
+    }
+    rc.files.push_back(std::move(fi));
+  }
+  // Object sizes + the manifest cross-checks of restore_checkpoint (format.cpp:446-470).
+  std::unordered_set<uint64_t> listed;
+  for (size_t k = 0; k < r.files.size(); ++k) {
+    std::unordered_set<uint64_t> expected(r.files[k].object_ids.begin(), r.files[k].object_ids.end());
+    std::unordered_set<uint64_t> found;
+    for (const auto& e : rc.files[k].entries) {
+      if (!expected.count(e.object_id))
+        fail(TS_ERR_BAD_MANIFEST, "file contains an object the manifest does not list",
+             static_cast<int64_t>(e.object_id));
+      found.insert(e.object_id);
+      rc.sizes[e.object_id] += e.length;
+      rc.kinds[e.object_id] = e.kind;
+    }
+    for (uint64_t oid : r.files[k].object_ids)
+      if (!found.count(oid))
+        fail(TS_ERR_CORRUPT_FOOTER, "file is missing manifest-listed objects: " + rc.files[k].path,
+             static_cast<int64_t>(oid));
+  }
+  for (const auto& o : r.objects)
+    if (!rc.sizes.count(o.object_id))
+      fail(TS_ERR_BAD_MANIFEST, "object missing from checkpoint", static_cast<int64_t>(o.object_id));
+  rc.loaded = true;
+}
+
+restore_handle::restore_handle(const std::string& manifest_path) {
+  m = read_manifest(manifest_path);
+  const auto slash = manifest_path.find_last_of('/');
+  base = slash == std::string::npos ? "." : manifest_path.substr(0, slash);
+  ranks.resize(m.ranks.size());
+}
+
+namespace {
+// Pieces of one object sorted by object offset must tile [0, size) (format.cpp:269-278).
+void check_tiling(std::vector<const footer_entry*>& pieces, uint64_t oid) {
+  std::sort(pieces.begin(), pieces.end(),
+            [](const footer_entry* a, const footer_entry* b) { return a->object_offset_base < b->object_offset_base; });
+  uint64_t off = 0;
+  for (const auto* e : pieces) {
+    if (e->object_offset_base != off)
+      fail(TS_ERR_CORRUPT_FOOTER, "gap in object byte ranges", static_cast<int64_t>(oid));
+    off += e->length;
+  }
+}
+}  // namespace
+
+void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n, int device,
+                                  cudaStream_t st, ts_restore_stats* stats) {
+  const int64_t t_begin = now_ns();
+  load_rank(index);
+  auto& rc = ranks[static_cast<size_t>(index)];
+  const auto& mr = m.ranks[static_cast<size_t>(index)];
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+
+  std::unordered_map<uint64_t, const ts_object_desc*> dmap;
+  for (size_t i = 0; i < n; ++i) dmap.emplace(dst[i].object_id, &dst[i]);
+
+  // Image = each file's region [4096, region_end), 4 KiB aligned file images.
+  struct rpiece {
+    uint64_t pos, len;
+    uint32_t obj;  // index into objs
+    uint64_t obj_off;
+  };
+  struct robj {
+    uint64_t oid, size, ck;
+    const ts_object_desc* d;
+    uint64_t fnv = fnv_seed, hashed = 0;
+    bool busy = false;
+    std::deque<std::pair<const uint8_t*, std::pair<uint64_t, int>>> q;  // ptr, (len, slot)
+  };
+  std::vector<robj> objs;
+  std::vector<rpiece> pieces;
+  std::vector<std::pair<uint64_t, uint64_t>> file_img;  // (img start, len)
+  std::unordered_map<uint64_t, uint32_t> oidx;
+  uint64_t img = 0, raw_bytes = 0;
+  for (size_t k = 0; k < rc.files.size(); ++k) {
+    const auto& fi = rc.files[k];
+    img = align_up(img, 4096);
+    const uint64_t fimg = img;
+    file_img.push_back({fimg, fi.region_end - header_reserved});
+    std::unordered_map<uint64_t, std::vector<const footer_entry*>> by_obj;
+    for (const auto& e : fi.entries)
+      if (e.kind == 0) by_obj[e.object_id].push_back(&e);
+    for (auto& [oid, ps] : by_obj) {
+      check_tiling(ps, oid);
+      auto it = dmap.find(oid);
+      if (it == dmap.end())
+        fail(TS_ERR_INVALID_ARG, "restore: no destination for raw object", static_cast<int64_t>(oid));
+      if (it->second->size_bytes != rc.sizes[oid])
+        fail(TS_ERR_INVALID_ARG, "restore: destination size mismatch", static_cast<int64_t>(oid));
+      robj o;
+      o.oid = oid;
+      o.size = rc.sizes[oid];
+      o.ck = ps.front()->checksum;
+      o.d = it->second;
+      oidx[oid] = static_cast<uint32_t>(objs.size());
+      for (const auto* e : ps)
+        pieces.push_back({fimg + (e->file_offset - header_reserved), e->length,
+                          static_cast<uint32_t>(objs.size()), e->object_offset_base});
+      objs.push_back(std::move(o));
+      raw_bytes += rc.sizes[oid];
+    }
+    img = fimg + (fi.region_end - header_reserved);
+  }
+  std::sort(pieces.begin(), pieces.end(), [](const rpiece& a, const rpiece& b) { return a.pos < b.pos; });
+
+  // Device scatter table (device-tier destinations only).
+  std::vector<dev::useg> usegs;
+  for (const auto& p : pieces) {
+    const auto& o = objs[p.obj];
+    if (o.d->tier == TS_TIER_DEVICE)
+      usegs.push_back({p.pos, p.len, static_cast<uint8_t*>(const_cast<void*>(o.d->data)) + p.obj_off});
+  }
+
+  const uint64_t W = 64ull << 20;
+  const int K = 4;
+  uint8_t* hring;
+  {
+    std::lock_guard<std::mutex> g(g_stage_mu);
+    hring = pinned_stage(W * K);
+  }
+  std::lock_guard<std::mutex> stage_guard(g_stage_mu);  // one restore at a time uses the ring
+  uint8_t* dring = nullptr;
+  dev::useg* d_usegs = nullptr;
+  cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&dring), W * K, st), "cudaMallocAsync(restore ring)");
+  if (!usegs.empty()) {
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d_usegs), usegs.size() * sizeof(dev::useg), st), "alloc");
+    cuda_check(cudaMemcpyAsync(d_usegs, usegs.data(), usegs.size() * sizeof(dev::useg),
+                               cudaMemcpyHostToDevice, st), "upload unpack table");
+  }
+  cudaEvent_t ev_a, ev_b;
+  cudaEventCreate(&ev_a);
+  cudaEventCreate(&ev_b);
+
+  std::vector<fd_holder> fds(rc.files.size());
+  for (size_t k = 0; k < rc.files.size(); ++k) {
+    fds[k].fd = ::open(rc.files[k].path.c_str(), O_RDONLY);
+    if (fds[k].fd < 0) fail(TS_ERR_MISSING_FILE, "cannot open " + rc.files[k].path);
+  }
+
+  struct shared_state {
+    std::mutex mu;
+    std::condition_variable cv;
+    int slot_refs[4] = {0, 0, 0, 0};
+    std::string err;
+    ts_status err_status = TS_OK;
+    int64_t err_oid = -1;
+  } S;
+  const int nthreads = static_cast<int>(std::min<unsigned>(16, std::max(2u, std::thread::hardware_concurrency())));
+  thread_pool pool(nthreads);
+  auto set_err = [&](const error& e) {
+    std::lock_guard<std::mutex> g(S.mu);
+    if (S.err_status == TS_OK) {
+      S.err_status = e.status;
+      S.err = e.what();
+      S.err_oid = e.object_id;
+    }
+  };
+  auto release = [&](int slot) {
+    std::lock_guard<std::mutex> g(S.mu);
+    if (--S.slot_refs[slot] == 0) S.cv.notify_all();
+  };
+  std::function<void(uint32_t)> hash_obj = [&](uint32_t oi) {
+    auto& o = objs[oi];
+    for (;;) {
+      std::pair<const uint8_t*, std::pair<uint64_t, int>> p;
+      {
+        std::lock_guard<std::mutex> g(S.mu);
+        if (o.q.empty()) {
+          o.busy = false;
+          return;
+        }
+        p = o.q.front();
+        o.q.pop_front();
+      }
+      o.fnv = fnv1a64(p.first, p.second.first, o.fnv);
+      o.hashed += p.second.first;
+      release(p.second.second);
+    }
+  };
+  struct host_cb_arg {
+    shared_state* s;
+    int slot;
+  };
+  std::vector<host_cb_arg> cb_args(K);
+  for (int k = 0; k < K; ++k) cb_args[k] = {&S, k};
+
+  double read_s = 0;
+  cuda_check(cudaEventRecord(ev_a, st), "event");
+  size_t pi = 0, ui = 0;
+  uint32_t launches = 0;
+  const int ctas = dev::sm_count(device) * 2;
+  for (uint64_t lo = 0, w = 0; lo < img; lo += W, ++w) {
+    const uint64_t hi = std::min(lo + W, img);
+    const int slot = static_cast<int>(w % K);
+    uint8_t* hs = hring + static_cast<uint64_t>(slot) * W;
+    {
+      std::unique_lock<std::mutex> g(S.mu);
+      S.cv.wait(g, [&] { return S.slot_refs[slot] == 0; });
+      if (S.err_status != TS_OK) break;
+    }
+    // Parallel pread of the window's file ranges (<= 8 MiB per task).
+    const int64_t r0 = now_ns();
+    {
+      std::mutex lm;
+      std::condition_variable lcv;
+      int outstanding = 0;
+      for (size_t k = 0; k < rc.files.size(); ++k) {
+        const uint64_t a = std::max(lo, file_img[k].first);
+        const uint64_t b = std::min(hi, file_img[k].first + file_img[k].second);
+        for (uint64_t x = a; x < b; x += (8ull << 20)) {
+          const uint64_t y = std::min<uint64_t>(b, x + (8ull << 20));
+          {
+            std::lock_guard<std::mutex> g(lm);
+            ++outstanding;
+          }
+          pool.submit([&, k, x, y] {
+            try {
+              pread_all(fds[k].fd, hs + (x - lo), y - x, header_reserved + (x - file_img[k].first), rc.files[k].path);
+            } catch (const error& e) {
+              set_err(e);
+            }
+            std::lock_guard<std::mutex> g(lm);
+            if (--outstanding == 0) lcv.notify_all();
+          });
+        }
+      }
+      std::unique_lock<std::mutex> g(lm);
+      lcv.wait(g, [&] { return outstanding == 0; });
+    }
+    read_s += (now_ns() - r0) * 1e-9;
+    // H2D + scatter-unpack of the window on the restore stream.
+    {
+      std::lock_guard<std::mutex> g(S.mu);
+      S.slot_refs[slot] += 1;  // released by the stream callback
+    }
+    uint8_t* ds = dring + static_cast<uint64_t>(slot) * W;
+    cuda_check(cudaMemcpyAsync(ds, hs, hi - lo, cudaMemcpyHostToDevice, st), "H2D window");
+    while (ui < usegs.size() && usegs[ui].pos + usegs[ui].len <= lo) ++ui;
+    if (ui < usegs.size() && usegs[ui].pos < hi) {
+      dev::launch_unpack(d_usegs + ui, static_cast<uint32_t>(usegs.size() - ui), lo, hi, ds, ctas, 512, st);
+      launches += 1;
+      cuda_check(cudaGetLastError(), "unpack launch");
+    }
+    cuda_check(cudaLaunchHostFunc(st, [](void* a) {
+                 auto* p = static_cast<host_cb_arg*>(a);
+                 std::lock_guard<std::mutex> g(p->s->mu);
+                 if (--p->s->slot_refs[p->slot] == 0) p->s->cv.notify_all();
+               }, &cb_args[slot]), "cudaLaunchHostFunc");
+    // Checksum pieces (object order preserved: windows are visited in order).
+    while (pi < pieces.size() && pieces[pi].pos + pieces[pi].len <= lo) ++pi;
+    std::vector<uint32_t> sched;
+    for (size_t q = pi; q < pieces.size() && pieces[q].pos < hi; ++q) {
+      const auto& p = pieces[q];
+      const uint64_t a = std::max(lo, p.pos), b = std::min(hi, p.pos + p.len);
+      if (b <= a) continue;
+      auto& o = objs[p.obj];
+      if (o.d->tier != TS_TIER_DEVICE)
+        std::memcpy(static_cast<uint8_t*>(const_cast<void*>(o.d->data)) + p.obj_off + (a - p.pos), hs + (a - lo), b - a);
+      std::lock_guard<std::mutex> g(S.mu);
+      S.slot_refs[slot] += 1;
+      o.q.push_back({hs + (a - lo), {b - a, slot}});
+      if (!o.busy) {
+        o.busy = true;
+        sched.push_back(p.obj);
+      }
+    }
+    for (uint32_t oi : sched) pool.submit([&, oi] { hash_obj(oi); });
+  }
+  {
+    std::unique_lock<std::mutex> g(S.mu);
+    S.cv.wait(g, [&] {
+      for (int k = 0; k < K; ++k)
+        if (S.slot_refs[k]) return false;
+      return true;
+    });
+  }
+  cuda_check(cudaEventRecord(ev_b, st), "event");
+  cuda_check(cudaStreamSynchronize(st), "restore stream");
+  float h2d_ms = 0;
+  cudaEventElapsedTime(&h2d_ms, ev_a, ev_b);
+  cudaEventDestroy(ev_a);
+  cudaEventDestroy(ev_b);
+  cudaFreeAsync(dring, st);
+  if (d_usegs) cudaFreeAsync(d_usegs, st);
+  cudaStreamSynchronize(st);
+  if (S.err_status != TS_OK) throw error(S.err_status, S.err, S.err_oid);
+  const int64_t t_verify = now_ns();
+  for (const auto& o : objs)
+    if (o.hashed != o.size || o.fnv != o.ck)
+      fail(TS_ERR_CORRUPT_OBJECT, "checksum mismatch for object " + std::to_string(o.oid), static_cast<int64_t>(o.oid));
+
+  // Structured objects: append-region pieces, checksum, decode (format.cpp:479-489).
+  uint64_t ser_bytes = 0;
+  for (size_t k = 0; k < rc.files.size(); ++k) {
+    std::unordered_map<uint64_t, std::vector<const footer_entry*>> by_obj;
+    for (const auto& e : rc.files[k].entries)
+      if (e.kind != 0) by_obj[e.object_id].push_back(&e);
+    for (auto& [oid, ps] : by_obj) {
+      check_tiling(ps, oid);
+      std::vector<uint8_t> bytes;
+      for (const auto* e : ps) {
+        const size_t at = bytes.size();
+        bytes.resize(at + e->length);
+        pread_all(fds[k].fd, bytes.data() + at, e->length, e->file_offset, rc.files[k].path);
+      }
+      if (fnv1a64(bytes.data(), bytes.size()) != ps.front()->checksum)
+        fail(TS_ERR_CORRUPT_OBJECT, "checksum mismatch for object " + std::to_string(oid),
+             static_cast<int64_t>(oid));
+      try {
+        rc.structured[oid] = decode(bytes.data(), bytes.size());
+      } catch (const error& e) {
+        fail(TS_ERR_CORRUPT_OBJECT, std::string("structured object does not decode: ") + e.what(),
+             static_cast<int64_t>(oid));
+      }
+      ser_bytes += bytes.size();
+    }
+  }
+  (void)mr;
+  if (stats) {
+    stats->bytes = raw_bytes + ser_bytes;
+    stats->read_s = read_s;
+    stats->verify_s = (now_ns() - t_verify) * 1e-9;
+    stats->h2d_unpack_s = h2d_ms * 1e-3;
+    stats->h2d_ms = h2d_ms;
+    stats->unpack_ms = 0;
+    stats->total_s = (now_ns() - t_begin) * 1e-9;
+    stats->kernel_launches = launches;
+  }
+}
+
+// verify_checkpoint (format.cpp:496-529): full checksum pass, never throws.
+void verify_checkpoint(const std::string& manifest_path, std::vector<std::pair<int, int64_t>>& issues,
+                       uint64_t& files_checked, uint64_t& objects_checked) {
+  files_checked = objects_checked = 0;
+  manifest m;
+  try {
+    m = read_manifest(manifest_path);
+  } catch (const error& e) {
+    issues.push_back({e.status, e.object_id});
+    return;
+  }
+  const auto slash = manifest_path.find_last_of('/');
+  const std::string base = slash == std::string::npos ? "." : manifest_path.substr(0, slash);
+  std::mutex mu;
+  {
+    thread_pool pool(static_cast<int>(std::min<unsigned>(16, std::max(2u, std::thread::hardware_concurrency()))));
+    for (const auto& r : m.ranks) {
+      for (const auto& mf : r.files) {
+        pool.submit([&, path = base + "/" + mf.path, oids = mf.object_ids] {
+          std::vector<std::pair<int, int64_t>> local;
+          uint64_t nobj = 0;
+          bool file_ok = false;
+          try {
+            uint64_t size = 0;
+            auto entries = read_footer(path, &size);
+            fd_holder fd;
+            fd.fd = ::open(path.c_str(), O_RDONLY);
+            if (fd.fd < 0) fail(TS_ERR_MISSING_FILE, "cannot open " + path);
+            std::map<uint64_t, std::vector<const footer_entry*>> by_obj;
+            for (const auto& e : entries) {
+              if (e.file_offset + e.length > size)
+                fail(TS_ERR_CORRUPT_FOOTER, "entry range outside the file", static_cast<int64_t>(e.object_id));
+              by_obj[e.object_id].push_back(&e);
+            }
+            std::vector<uint8_t> buf(8ull << 20);
+            for (auto& [oid, ps] : by_obj) {
+              check_tiling(ps, oid);
+              uint64_t h = fnv_seed;
+              for (const auto* e : ps) {
+                for (uint64_t x = 0; x < e->length; x += buf.size()) {
+                  const uint64_t len = std::min<uint64_t>(buf.size(), e->length - x);
+                  pread_all(fd.fd, buf.data(), len, e->file_offset + x, path);
+                  h = fnv1a64(buf.data(), len, h);
+                }
+              }
+              if (h != ps.front()->checksum)
+                fail(TS_ERR_CORRUPT_OBJECT, "checksum mismatch for object " + std::to_string(oid),
+                     static_cast<int64_t>(oid));
+            }
+            nobj = by_obj.size();
+            file_ok = true;
+            for (uint64_t oid : oids)
+              if (!by_obj.count(oid)) local.push_back({TS_ERR_CORRUPT_FOOTER, static_cast<int64_t>(oid)});
+          } catch (const error& e) {
+            local.push_back({e.status, e.object_id});
+          }
+          std::lock_guard<std::mutex> g(mu);
+          if (file_ok) {
+            files_checked += 1;
+            objects_checked += nobj;
+          }
+          issues.insert(issues.end(), local.begin(), local.end());
+        });
+      }
+    }
+  }
+}
+
+}  // namespace tsb

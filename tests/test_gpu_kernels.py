@@ -1,0 +1,116 @@
+"""sm_100a kernels against the oracle: pattern fill/verify, gather-pack (device
+and zero-copy host destinations), scatter-unpack. Integer/byte work: bit-exact."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _descs(native, items):
+    arr = (native.PatternDesc * len(items))()
+    for i, (ptr, size, space, off) in enumerate(items):
+        arr[i].data, arr[i].size, arr[i].space, arr[i].offset = ptr, size, space, off
+    return arr
+
+
+def test_pattern_fill_matches_oracle(gpu, native, oracle):
+    rng = np.random.default_rng(3)
+    buf = torch.zeros(1 << 22, dtype=torch.uint8, device=gpu)
+    items, pos = [], 1
+    for k in range(60):
+        size = int(rng.choice([1, 2, 7, 15, 16, 17, 4095, 65536 + 3, int(rng.integers(1, 50000))]))
+        off = int(rng.integers(0, 1 << 40))
+        space = int(rng.integers(0, 1 << 62))
+        items.append((buf.data_ptr() + pos, size, space, off))
+        pos += size + int(rng.integers(0, 40))
+    arr = _descs(native, items)
+    native.call(native.lib.ts_pattern_fill, arr, len(items), 42, 9, None)
+    torch.cuda.synchronize()
+    host = buf.cpu().numpy()
+    base = buf.data_ptr()
+    for ptr, size, space, off in items:
+        got = host[ptr - base: ptr - base + size]
+        assert (got == oracle.fill_pattern(size, 42, space, 9, off)).all()
+    mism = C.c_uint64()
+    native.call(native.lib.ts_pattern_verify, arr, len(items), 42, 9, None, C.byref(mism))
+    assert mism.value == 0
+    buf[items[5][0] - base] ^= 0xFF
+    buf[items[30][0] - base + items[30][1] - 1] ^= 0x01
+    native.call(native.lib.ts_pattern_verify, arr, len(items), 42, 9, None, C.byref(mism))
+    assert mism.value == 2
+    native.call(native.lib.ts_pattern_verify, arr, len(items), 42, 10, None, C.byref(mism))
+    assert mism.value > 0.9 * sum(i[1] for i in items)
+
+
+def _fragments(gpu, rng, n, max_size):
+    src = torch.randint(0, 256, (n * max_size + 4096,), dtype=torch.uint8, device=gpu)
+    frags, pos = [], 0
+    for _ in range(n):
+        size = int(rng.choice([1, 3, 16, 31, 4096, int(rng.integers(1, max_size))]))
+        pos += int(rng.integers(0, 33))
+        frags.append((pos, size))
+        pos += size
+    return src, frags
+
+
+@pytest.mark.parametrize("dst_kind", ["device", "host"])
+def test_pack_matches_numpy(gpu, native, dst_kind):
+    rng = np.random.default_rng(11 if dst_kind == "device" else 12)
+    src, frags = _fragments(gpu, rng, 300, 70_000)
+    n = len(frags)
+    offs, cur = [], 0
+    for _, size in frags:
+        cur = (cur + 4095) // 4096 * 4096 if rng.random() < 0.7 else cur + int(rng.integers(0, 5))
+        offs.append(cur)
+        cur += size
+    dst_len = cur + 123
+    if dst_kind == "device":
+        dst = torch.full((dst_len,), 0xAB, dtype=torch.uint8, device=gpu)
+    else:
+        dst = torch.full((dst_len,), 0xAB, dtype=torch.uint8).pin_memory()
+    srcs = (C.c_void_p * n)(*[src.data_ptr() + p for p, _ in frags])
+    sizes = (C.c_uint64 * n)(*[s for _, s in frags])
+    doffs = (C.c_uint64 * n)(*offs)
+    native.call(native.lib.ts_pack, srcs, sizes, doffs, n, dst.data_ptr(), dst_len, 0, 0, None)
+    torch.cuda.synchronize()
+    s = src.cpu().numpy()
+    exp = np.zeros(dst_len, dtype=np.uint8)
+    for (p, size), o in zip(frags, offs):
+        exp[o:o + size] = s[p:p + size]
+    got = dst.cpu().numpy()
+    assert (got == exp).all()
+
+
+def test_unpack_roundtrip(gpu, native):
+    rng = np.random.default_rng(5)
+    img_len = 3 << 20
+    img = torch.randint(0, 256, (img_len,), dtype=torch.uint8, device=gpu)
+    out = torch.zeros(img_len + (1 << 14), dtype=torch.uint8, device=gpu)
+    pieces, pos, dpos = [], 0, 1
+    while pos < img_len - 100_000:
+        size = int(rng.integers(1, 90_000))
+        pos += int(rng.integers(0, 4000))
+        dpos += int(rng.integers(0, 7))
+        pieces.append((pos, size, dpos))
+        pos += size
+        dpos += size
+    n = len(pieces)
+    so = (C.c_uint64 * n)(*[p for p, _, _ in pieces])
+    dsts = (C.c_void_p * n)(*[out.data_ptr() + d for _, _, d in pieces])
+    sizes = (C.c_uint64 * n)(*[s for _, s, _ in pieces])
+    native.call(native.lib.ts_unpack, img.data_ptr(), so, dsts, sizes, n, 0, 0, None)
+    torch.cuda.synchronize()
+    a, b = img.cpu().numpy(), out.cpu().numpy()
+    for p, s, d in pieces:
+        assert (b[d:d + s] == a[p:p + s]).all()
+
+
+def test_kernel_launches_counted(gpu, native):
+    before = native.lib.ts_kernel_launch_count()
+    buf = torch.zeros(1000, dtype=torch.uint8, device=gpu)
+    arr = _descs(native, [(buf.data_ptr(), 1000, 1, 0)])
+    native.call(native.lib.ts_pattern_fill, arr, 1, 1, 1, None)
+    assert native.lib.ts_kernel_launch_count() == before + 1

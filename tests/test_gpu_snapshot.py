@@ -1,0 +1,151 @@
+"""Parity of the B200 snapshot path with the reference: checkpoint trees written
+by the GPU engine are byte-identical to the trees the compiled reference wrote
+for the same state (tests/golden/trees), in every D2H mode, with windows and
+staging pools small enough to force multi-window pipelines and back-pressure."""
+import json
+import os
+import shutil
+import subprocess
+
+import pytest
+import torch
+
+from conftest import GOLDEN, ROOT, golden_recipes, read_tree
+from gpu_helpers import checkpoint_recipe
+from paper_2601_16956_b200 import api
+from paper_2601_16956_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+MODES = ["ring", "direct", "zerocopy"]
+
+
+def cfg_for(mode, **kw):
+    base = dict(d2h_mode=mode, raw_chunk_bytes=64 << 10, staging_capacity_bytes=1 << 20,
+                device_staging_bytes=256 << 10, flush_workers=3)
+    base.update(kw)
+    return api.EngineConfig(**base)
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("name", golden_recipes())
+def test_snapshot_bytes_equal_reference(gpu, tmp_path, name, mode):
+    rec = S.load_recipe(os.path.join(GOLDEN, "recipes", name + ".recipe"))
+    out = str(tmp_path / "ckpt")
+    _, states, stats, _ = checkpoint_recipe(rec, out, cfg_for(mode))
+    assert read_tree(out) == read_tree(os.path.join(GOLDEN, "trees", name))
+    # the capture never modifies the state
+    for st in states:
+        assert api.pattern_mismatches(st, rec.pit) == 0
+    for s in stats:
+        assert s["snapshot_done"] and s["persisted_done"] and not s["failed"]
+
+
+@pytest.mark.parametrize("strategy", ["sync", "two_phase", "lazy"])
+def test_strategies_identical(gpu, tmp_path, strategy):
+    name = "hand_mixed"
+    rec = S.load_recipe(os.path.join(GOLDEN, "recipes", name + ".recipe"))
+    out = str(tmp_path / strategy)
+    checkpoint_recipe(rec, out, cfg_for("ring", strategy=strategy))
+    assert read_tree(out) == read_tree(os.path.join(GOLDEN, "trees", name))
+
+
+def test_shadow_ring_and_window_sizes(gpu, tmp_path):
+    """Full device shadow, 2-slot ring, 1-window pool and huge windows agree."""
+    name = "zero3_tiny"
+    rec = S.load_recipe(os.path.join(GOLDEN, "recipes", name + ".recipe"))
+    ref = read_tree(os.path.join(GOLDEN, "trees", name))
+    for i, kw in enumerate([dict(device_staging_bytes=1 << 30, raw_chunk_bytes=16 << 20, staging_capacity_bytes=64 << 20),
+                            dict(device_staging_bytes=8 << 10, raw_chunk_bytes=4096, staging_capacity_bytes=4096),
+                            dict(raw_chunk_bytes=10_000, staging_capacity_bytes=30_000, flush_workers=1)]):
+        out = str(tmp_path / str(i))
+        checkpoint_recipe(rec, out, cfg_for("ring", **kw))
+        assert read_tree(out) == ref, kw
+
+
+def test_consecutive_checkpoints_and_checksums(gpu, tmp_path, oracle):
+    """Three lazy checkpoints of one rank through one engine with updates in
+    between (run_training's loop): each checkpoint holds its own iteration."""
+    rec = S.load_recipe(os.path.join(GOLDEN, "recipes", "odd_layout.recipe"))
+    spec = rec.ranks[1]
+    st = api.materialize_payloads(spec, 0, 0)
+    eng = api.CheckpointEngine(cfg_for("ring"), spec.rank_id, 0)
+    pending = None
+    for it in range(1, 4):
+        eng.pre_update_barrier(pending, host_block=1)
+        api.mutate_update_step(st, it)
+        sess = api.CheckpointSession(str(tmp_path / f"c{it}"), it, it, None, n_ranks=1)
+        pending = eng.issue_checkpoint(sess, st, it)
+        pending.wait_persisted()
+        sess.wait_complete(30)
+        for o in spec.objects:
+            if o.kind == 0:
+                exp = oracle.fnv1a64(oracle.fill_pattern(o.size, spec.seed, o.space, it, o.offset))
+                assert pending.object_checksum(o.object_id) == exp
+        restored = oracle.restore_checkpoint(str(tmp_path / f"c{it}" / "MANIFEST.tlv"))
+        assert restored[0]["objects"][spec.objects[-1].object_id]["iteration"] == it
+    eng.shutdown()
+
+
+def test_lazy_barrier_is_load_bearing(gpu, tmp_path):
+    """With the pre-update barrier (stream wait, no host block) an update issued
+    right after the checkpoint cannot leak into it; skipping the barrier lets it
+    leak (the reference's skip_update_barrier negative test, simulator.hpp:81-83)."""
+    spec = S.RankSpec(0, seed=3, metadata_bytes=100)
+    spec.objects = [S.ObjSpec(1, 0, 0, 1, 1, 64 << 20, S.pack_space(2, 0, 0), 0),
+                    S.ObjSpec(2, 1, 1, 2, 0, meta=("meta",))]
+    prod = torch.cuda.Stream()
+    st = api.materialize_payloads(spec, 0, 1, stream=prod)
+    eng = api.CheckpointEngine(cfg_for("ring", device_staging_bytes=8 << 20, raw_chunk_bytes=4 << 20,
+                                       staging_capacity_bytes=16 << 20), 0, 0)
+    for use_barrier in (True, False):
+        with torch.cuda.stream(prod):
+            torch.cuda._sleep(200_000_000)  # the producer is still busy at issue time
+        sess = api.CheckpointSession(str(tmp_path / str(use_barrier)), 1, 1, None, 1)
+        t = eng.issue_checkpoint(sess, st, 1, producer_stream=prod)
+        upd = torch.cuda.Stream()
+        if use_barrier:
+            eng.pre_update_barrier(t, stream=upd, host_block=0)
+        api.mutate_update_step(st, 2, stream=upd)
+        t.wait_persisted()
+        sess.wait_complete(30)
+        r = api.restore_checkpoint(str(tmp_path / str(use_barrier) / "MANIFEST.tlv"))[0]
+        raw = [o for o in r.objects if o.is_raw()][0]
+        raw.pattern_space, raw.pattern_offset = spec.objects[0].space, 0
+        r.seed = spec.seed
+        bad = api.pattern_mismatches(r, 1)
+        if use_barrier:
+            assert bad == 0
+        else:
+            assert bad > 0
+        torch.cuda.synchronize()
+        api.mutate_update_step(st, 1)
+        torch.cuda.synchronize()
+    eng.shutdown()
+
+
+def test_reference_restores_our_checkpoint(gpu, tmp_path):
+    """The unmodified reference (oracle/_ref/ts_ref_driver) verifies and restores a
+    checkpoint written by the B200 engine, with identical object checksums."""
+    drv = os.path.join(ROOT, "oracle", "_ref", "ts_ref_driver")
+    if not os.path.exists(drv):
+        pytest.skip("oracle/_ref not built")
+    rec = S.zero3_recipe("z", S.llama_tensors(96, 200, 3, vocab=300), 3, seed=5, metadata_bytes=5000,
+                         iteration=4)
+    out = str(tmp_path / "ours")
+    _, _, stats, _ = checkpoint_recipe(rec, out, cfg_for("ring"))
+    v = json.loads(subprocess.run([drv, "verify", out + "/MANIFEST.tlv"], capture_output=True, text=True,
+                                  check=True).stdout)
+    assert v["ok"] and v["objects"] == sum(len(r.objects) for r in rec.ranks)
+    r = json.loads(subprocess.run([drv, "restore", out + "/MANIFEST.tlv"], capture_output=True, text=True,
+                                  check=True).stdout)
+    assert r["ok"]
+
+
+def test_back_pressure_bounded_pool(gpu, tmp_path):
+    """Staging capacity far below the checkpoint: lazy still completes (SPEC
+    back-pressure property) and the bytes are unchanged."""
+    name = "tiny_layout"
+    rec = S.load_recipe(os.path.join(GOLDEN, "recipes", name + ".recipe"))
+    out = str(tmp_path / "bp")
+    checkpoint_recipe(rec, out, cfg_for("direct", staging_capacity_bytes=8192, raw_chunk_bytes=8192))
+    assert read_tree(out) == read_tree(os.path.join(GOLDEN, "trees", name))
