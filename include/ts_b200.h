@@ -165,6 +165,8 @@ typedef struct ts_engine_config {
   int32_t pack_threads;             /* threads per pack CTA, default 512 */
   int32_t low_priority_stream;      /* snapshot streams at the lowest priority, default 1 */
   int32_t write_files;              /* 0 = snapshot-only run (no file I/O, bench only) */
+  int32_t checksum_on_gpu;          /* 1 (default): exact segment-parallel FNV-1a kernels on the
+                                       device copy; 0: host threads over the pinned pool */
 } ts_engine_config;
 
 void ts_engine_config_default(ts_engine_config* cfg);
@@ -296,6 +298,12 @@ ts_status ts_pattern_fill(const ts_pattern_desc* d, size_t n, uint64_t seed, uin
 /* matches_pattern on device: *mismatched_bytes = total mismatching bytes (0 = bit-exact) */
 ts_status ts_pattern_verify(const ts_pattern_desc* d, size_t n, uint64_t seed,
                             uint64_t iteration, void* stream, uint64_t* mismatched_bytes);
+
+/* FNV-1a-64 of `n` device byte ranges, computed on the GPU (segment-parallel,
+ * exact). `init` (host, may be NULL = fresh seed) chains from prior states;
+ * results land in host `out`. Synchronous w.r.t. the host. */
+ts_status ts_fnv1a64_device(const void* const* ptrs, const uint64_t* sizes, size_t n,
+                            const uint64_t* init, uint64_t* out, void* stream);
 
 /* Raw kernel entry for microbenchmarks: gather `n` device fragments into `dst`
  * (device or mapped-host) at dst_offsets, zero-filling the gaps up to `dst_len`. */

@@ -99,7 +99,8 @@ class EngineConfigC(C.Structure):
                 ("alignment", C.c_uint64), ("cache_acquire_timeout_ns", C.c_int64),
                 ("overwrite", C.c_int32), ("d2h_mode", C.c_int32), ("device_staging_bytes", C.c_uint64),
                 ("hybrid_direct_min_bytes", C.c_uint64), ("pack_ctas", C.c_int32),
-                ("pack_threads", C.c_int32), ("low_priority_stream", C.c_int32), ("write_files", C.c_int32)]
+                ("pack_threads", C.c_int32), ("low_priority_stream", C.c_int32), ("write_files", C.c_int32),
+                ("checksum_on_gpu", C.c_int32)]
 
 
 class ManifestEcho(C.Structure):
@@ -211,6 +212,7 @@ _sig("ts_pattern_verify", i32, C.POINTER(PatternDesc), sz, u64, u64, P, C.POINTE
 _sig("ts_pack", i32, C.POINTER(P), C.POINTER(u64), C.POINTER(u64), sz, P, u64, i32, i32, P)
 _sig("ts_unpack", i32, P, C.POINTER(u64), C.POINTER(P), C.POINTER(u64), sz, i32, i32, P)
 _sig("ts_kernel_launch_count", u64)
+_sig("ts_fnv1a64_device", i32, C.POINTER(P), C.POINTER(u64), sz, C.POINTER(u64), C.POINTER(u64), P)
 
 def call(fn, *args):
     raise_for(fn(*args))

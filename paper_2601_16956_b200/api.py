@@ -155,6 +155,18 @@ def tlv_decode(b: bytes) -> Any:
     return Value.decode(b).to_py()
 
 
+def fnv1a64_device(tensors, init=None, stream=None):
+    """FNV-1a-64 of each device tensor's bytes, computed by the GPU kernels."""
+    n = len(tensors)
+    ptrs = (C.c_void_p * max(1, n))(*[t.data_ptr() for t in tensors])
+    sizes = (C.c_uint64 * max(1, n))(*[t.numel() * t.element_size() for t in tensors])
+    out = (C.c_uint64 * max(1, n))()
+    ini = (C.c_uint64 * max(1, n))(*init) if init is not None else None
+    sh = _stream_handle(stream)
+    N.call(N.lib.ts_fnv1a64_device, ptrs, sizes, n, ini, out, C.c_void_p(sh))
+    return list(out)[:n]
+
+
 def fnv1a64(data, state: int = 14695981039346656037) -> int:
     """FNV-1a-64 (common.hpp:44-51) of host bytes."""
     b = bytes(data)
@@ -243,6 +255,7 @@ class EngineConfig:
     pack_threads: int = 512
     low_priority_stream: bool = True
     write_files: bool = True
+    checksum_on_gpu: bool = True
 
     def to_c(self) -> N.EngineConfigC:
         c = N.EngineConfigC()
@@ -263,6 +276,7 @@ class EngineConfig:
         c.pack_threads = self.pack_threads
         c.low_priority_stream = int(self.low_priority_stream)
         c.write_files = int(self.write_files)
+        c.checksum_on_gpu = int(self.checksum_on_gpu)
         return c
 
 
@@ -451,7 +465,7 @@ def materialize_payloads(spec: RankSpec, device: int = 0, iteration: int = 0, st
     dev = torch.device("cuda", device)
     total, offs = 0, []
     for o in spec.objects:
-        if o.kind == 0:
+        if o.kind == 0 and o.tier == TIER_DEVICE:
             total = _align(total, max(1, o.align))
             offs.append(total)
             total += o.size
@@ -465,7 +479,10 @@ def materialize_payloads(spec: RankSpec, device: int = 0, iteration: int = 0, st
         so = StateObject(o.object_id, o.kind, o.tier if o.kind == 0 else TIER_HOST, o.precision, o.file_id,
                          o.size, o.space, o.offset)
         if o.kind == 0:
-            so.payload = arena[off:off + o.size]
+            # device-tier shards are views of the HBM arena; host-tier ones live
+            # in pinned host memory (the pattern kernel writes them through UVA)
+            so.payload = arena[off:off + o.size] if off is not None else \
+                torch.empty(o.size, dtype=torch.uint8).pin_memory()
         so._meta = o.meta  # type: ignore[attr-defined]
         rs.objects.append(so)
     mutate_update_step(rs, iteration, stream)

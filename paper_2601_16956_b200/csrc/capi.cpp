@@ -193,6 +193,7 @@ void ts_engine_config_default(ts_engine_config* c) {
   c->pack_threads = 512;
   c->low_priority_stream = 1;
   c->write_files = 1;
+  c->checksum_on_gpu = 1;
 }
 
 ts_status ts_engine_create(const ts_engine_config* cfg, int rank_id, int device, ts_engine** out) {
@@ -543,5 +544,33 @@ ts_status ts_unpack(const void* src, const uint64_t* src_offsets, void* const* d
 }
 
 uint64_t ts_kernel_launch_count(void) { return dev::launches(); }
+
+ts_status ts_fnv1a64_device(const void* const* ptrs, const uint64_t* sizes, size_t n, const uint64_t* init,
+                            uint64_t* out, void* stream) {
+  return guard([&] {
+    require_device();
+    if (n == 0) return;
+    auto st = static_cast<cudaStream_t>(stream);
+    std::vector<dev::fnv_obj> objs(n);
+    std::vector<uint64_t> states(n);
+    uint64_t nseg = 0;
+    for (size_t i = 0; i < n; ++i) {
+      objs[i] = {static_cast<const uint8_t*>(ptrs[i]), sizes[i], nseg};
+      nseg += (sizes[i] + dev::kFnvSeg - 1) / dev::kFnvSeg;
+      states[i] = init ? init[i] : fnv_seed;
+    }
+    const uint64_t tb = dev::align_up_dev(n * sizeof(dev::fnv_obj), 256), sb = dev::align_up_dev(n * 8, 256);
+    uint8_t* buf = nullptr;
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&buf), tb + sb + dev::fnv_scratch_bytes(nseg, static_cast<uint32_t>(n)), st), "alloc");
+    cuda_check(cudaMemcpyAsync(buf, objs.data(), n * sizeof(dev::fnv_obj), cudaMemcpyHostToDevice, st), "upload");
+    cuda_check(cudaMemcpyAsync(buf + tb, states.data(), n * 8, cudaMemcpyHostToDevice, st), "upload");
+    dev::launch_fnv(reinterpret_cast<dev::fnv_obj*>(buf), static_cast<uint32_t>(n), nseg,
+                    reinterpret_cast<uint64_t*>(buf + tb), buf + tb + sb, st);
+    cuda_check(cudaGetLastError(), "fnv launch");
+    cuda_check(cudaMemcpyAsync(out, buf + tb, n * 8, cudaMemcpyDeviceToHost, st), "download");
+    cuda_check(cudaFreeAsync(buf, st), "free");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+  });
+}
 
 }  // extern "C"

@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <cerrno>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <unordered_set>
 
 namespace tsb {
@@ -15,6 +17,16 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 
 namespace {
+const bool g_trace = std::getenv("TS_TRACE") != nullptr;
+#define TRACE(...)                                                                     \
+  do {                                                                                 \
+    if (g_trace) {                                                                     \
+      std::fprintf(stderr, "[ts %lld] ", (long long)(now_ns() / 1000 % 100000000));    \
+      std::fprintf(stderr, __VA_ARGS__);                                               \
+      std::fprintf(stderr, "\n");                                                      \
+    }                                                                                  \
+  } while (0)
+
 void mkdirs(const std::string& path) {
   std::string cur;
   for (size_t i = 0; i <= path.size(); ++i) {
@@ -62,7 +74,13 @@ thread_pool::~thread_pool() {
 void thread_pool::submit(std::function<void()> f) {
   {
     std::lock_guard<std::mutex> g(mu_);
-    q_.push_back(std::move(f));
+    q_.push_back([f = std::move(f)] {
+      try {
+        f();
+      } catch (const std::exception& e) {
+        std::fprintf(stderr, "ts_b200: uncaught exception in worker task: %s\n", e.what());
+      }
+    });
   }
   cv_.notify_one();
 }
@@ -250,6 +268,12 @@ struct job {
   std::vector<cudaEvent_t> chunk_events;  // per-job, destroyed at the end
   uint64_t img = 0;
   bool io = true;
+  // device checksums (checksum_on_gpu): device-tier raw objects hashed by the
+  // FNV kernels; results land in a pool region
+  bool gpu_ck = false;
+  std::vector<uint32_t> fnv_objs;
+  pinned_pool::region fnv_r;
+  cudaEvent_t fnv_ev = nullptr;
 
   std::mutex mu;
   size_t wins_landed = 0, wins_enqueued = 0, structs_pending = 0, files_done = 0;
@@ -258,6 +282,23 @@ struct job {
 
 // ---------------------------------------------------------------------------
 // engine
+
+namespace {
+// Worker-task wrapper: a failure inside a task fails the ticket (and is
+// reported on the next wait) instead of terminating the process.
+template <class F>
+std::function<void()> guarded(const std::shared_ptr<job>& j, F&& f) {
+  return [j, f = std::forward<F>(f)]() mutable {
+    try {
+      f();
+    } catch (const error& e) {
+      j->t->fail(e.status, e.what(), e.object_id);
+    } catch (const std::exception& e) {
+      j->t->fail(TS_ERR_GENERIC, e.what());
+    }
+  };
+}
+}  // namespace
 
 engine::engine(const ts_engine_config& cfg, int rank_id, int device)
     : cfg_(cfg), rank_id_(rank_id), device_(device) {
@@ -285,6 +326,7 @@ engine::~engine() {
   cudaSetDevice(device_);
   if (ring_) cudaFree(ring_);
   if (segbuf_) cudaFree(segbuf_);
+  if (fnvbuf_) cudaFree(fnvbuf_);
   if (pack_stream_) cudaStreamDestroy(pack_stream_);
   if (copy_stream_) cudaStreamDestroy(copy_stream_);
   for (auto e : ev_free_) cudaEventDestroy(e);
@@ -342,6 +384,16 @@ uint8_t* engine::ensure_device_ring(uint64_t bytes) {
     ring_bytes_ = bytes;
   }
   return ring_;
+}
+
+uint8_t* engine::ensure_fnv_buffer(uint64_t bytes) {
+  if (fnvbuf_bytes_ < bytes) {
+    if (fnvbuf_) cudaFree(fnvbuf_);
+    fnvbuf_ = nullptr;
+    cuda_check(cudaMalloc(&fnvbuf_, bytes), "cudaMalloc(checksum scratch)");
+    fnvbuf_bytes_ = bytes;
+  }
+  return fnvbuf_;
 }
 
 void* engine::ensure_seg_buffer(uint64_t bytes) {
@@ -445,6 +497,11 @@ std::shared_ptr<ticket_state> engine::issue(session& s, const ts_rank_info& rank
     }
   }
 
+  j->gpu_ck = cfg_.checksum_on_gpu != 0;
+  if (j->gpu_ck)
+    for (size_t k = 0; k < j->raws.size(); ++k)
+      if (j->raws[k].device) j->fnv_objs.push_back(static_cast<uint32_t>(k));
+
   // D2H windows over [0, img) and their pieces (one sweep).
   const uint64_t W = std::min<uint64_t>(cfg_.raw_chunk_bytes, pool_->capacity());
   {
@@ -506,7 +563,7 @@ std::shared_ptr<ticket_state> engine::issue(session& s, const ts_rank_info& rank
   if (inline_ser) {
     for (size_t k = 0; k < j->sobjs.size(); ++k) serialize_task(j, k);
   } else {
-    for (size_t k = 0; k < j->sobjs.size(); ++k) workers_->submit([this, j, k] { serialize_task(j, k); });
+    for (size_t k = 0; k < j->sobjs.size(); ++k) workers_->submit(guarded(j, [this, j, k] { serialize_task(j, k); }));
   }
   {
     std::lock_guard<std::mutex> g(mu_);
@@ -591,6 +648,8 @@ void engine::run_job(const std::shared_ptr<job>& j) {
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   auto& t = *j->t;
   const int mode = cfg_.d2h_mode == TS_D2H_HYBRID ? TS_D2H_RING : cfg_.d2h_mode;
+  TRACE("run_job rank=%d mode=%d img=%llu wins=%zu segs=%zu", j->rank_id, mode, (unsigned long long)j->img,
+        j->wins.size(), j->segs.size());
   const int64_t timeout = cfg_.cache_acquire_timeout_ns;
   const int ctas = cfg_.pack_ctas > 0 ? cfg_.pack_ctas : sms_ * 2;
   const int threads = cfg_.pack_threads > 0 ? cfg_.pack_threads : 512;
@@ -620,30 +679,15 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     return t.failed;
   };
 
-  dev::seg* d_segs = nullptr;
-  if (j->img > 0 && mode != TS_D2H_DIRECT) {
-    d_segs = static_cast<dev::seg*>(ensure_seg_buffer(j->segs.size() * sizeof(dev::seg)));
-    // Upload before waiting on the producer (a pageable H2D syncs its stream).
-    cuda_check(cudaMemcpyAsync(d_segs, j->segs.data(), j->segs.size() * sizeof(dev::seg),
-                               cudaMemcpyHostToDevice, pack_stream_), "upload segment table");
-  }
-  cuda_check(cudaStreamWaitEvent(pack_stream_, t.ev_start, 0), "wait producer");
-  cuda_check(cudaStreamWaitEvent(copy_stream_, t.ev_start, 0), "wait producer");
-  cuda_check(cudaEventRecord(t.ev_pack0, mode == TS_D2H_DIRECT ? copy_stream_ : pack_stream_), "event");
-  if (j->img == 0) {
-    mark_capture(pack_stream_);
-    return;
-  }
-  const uint32_t nsegs = static_cast<uint32_t>(j->segs.size());
-  const uint64_t W = j->wins.front().hi - j->wins.front().lo;
-
-  if (mode == TS_D2H_RING) {
-    // HBM staging: whole image when it fits (device shadow), else two slots of
-    // whole windows, packs running ahead of the copies.
+  // Device staging plan (RING): whole image when it fits (device shadow), else
+  // two slots of whole windows with the packs running ahead of the copies.
+  const uint64_t W = j->wins.empty() ? 0 : j->wins.front().hi - j->wins.front().lo;
+  uint64_t chunk = 0;
+  int nslots = 0;
+  uint8_t* ring = nullptr;
+  if (mode == TS_D2H_RING && j->img > 0) {
     const uint64_t want = align_up(j->img, 256);
     const uint64_t cap = std::max<uint64_t>(cfg_.device_staging_bytes, 2 * W);
-    uint64_t chunk;
-    int nslots;
     if (cap >= want) {
       chunk = want;
       nslots = 1;
@@ -651,7 +695,69 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       chunk = std::max<uint64_t>(W, (cap / 2) / W * W);
       nslots = 2;
     }
-    uint8_t* ring = ensure_device_ring(nslots == 1 ? want : 2 * chunk);
+    ring = ensure_device_ring(nslots == 1 ? want : 2 * chunk);
+  }
+  const bool shadow = nslots == 1;
+
+  dev::seg* d_segs = nullptr;
+  if (j->img > 0 && mode != TS_D2H_DIRECT) {
+    d_segs = static_cast<dev::seg*>(ensure_seg_buffer(j->segs.size() * sizeof(dev::seg)));
+    // Upload before waiting on the producer (a pageable H2D syncs its stream).
+    cuda_check(cudaMemcpyAsync(d_segs, j->segs.data(), j->segs.size() * sizeof(dev::seg),
+                               cudaMemcpyHostToDevice, pack_stream_), "upload segment table");
+  }
+  // Device checksums: over the device shadow after the pack (off the capture
+  // path), else over the state itself before the capture completes.
+  const uint32_t nf = static_cast<uint32_t>(j->fnv_objs.size());
+  uint8_t* fbuf = nullptr;
+  uint64_t fnseg = 0, ftb = 0, fsb = 0;
+  if (nf) {
+    std::vector<dev::fnv_obj> fo(nf);
+    std::vector<uint64_t> st(nf, fnv_seed);
+    for (uint32_t i = 0; i < nf; ++i) {
+      const auto& r = j->raws[j->fnv_objs[i]];
+      fo[i] = {shadow ? ring + r.img : r.src, r.size, fnseg};
+      fnseg += (r.size + dev::kFnvSeg - 1) / dev::kFnvSeg;
+    }
+    ftb = align_up(nf * sizeof(dev::fnv_obj), 256);
+    fsb = align_up(nf * 8ull, 256);
+    fbuf = ensure_fnv_buffer(ftb + fsb + dev::fnv_scratch_bytes(fnseg, nf));
+    cuda_check(cudaMemcpyAsync(fbuf, fo.data(), nf * sizeof(dev::fnv_obj), cudaMemcpyHostToDevice, pack_stream_),
+               "upload checksum table");
+    cuda_check(cudaMemcpyAsync(fbuf + ftb, st.data(), nf * 8ull, cudaMemcpyHostToDevice, pack_stream_),
+               "upload checksum seeds");
+    j->fnv_r = pool_->acquire(nf * 8ull, timeout >= 0 ? now_ns() + timeout : -1);
+    j->fnv_ev = get_event();
+  }
+  auto launch_checksums = [&] {
+    dev::launch_fnv(reinterpret_cast<dev::fnv_obj*>(fbuf), nf, fnseg, reinterpret_cast<uint64_t*>(fbuf + ftb),
+                    fbuf + ftb + fsb, pack_stream_);
+    t.kernel_launches += 6;
+    cuda_check(cudaGetLastError(), "checksum kernels");
+    cuda_check(cudaMemcpyAsync(pool_->data(j->fnv_r), fbuf + ftb, nf * 8ull, cudaMemcpyDeviceToHost, pack_stream_),
+               "checksums D2H");
+    cuda_check(cudaEventRecord(j->fnv_ev, pack_stream_), "event");
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      inflight_.push_back({j, 0, true});
+    }
+    cv_.notify_all();
+  };
+  cuda_check(cudaStreamWaitEvent(pack_stream_, t.ev_start, 0), "wait producer");
+  cuda_check(cudaStreamWaitEvent(copy_stream_, t.ev_start, 0), "wait producer");
+  cuda_check(cudaEventRecord(t.ev_pack0, mode == TS_D2H_DIRECT ? copy_stream_ : pack_stream_), "event");
+  if (nf && !shadow) {
+    launch_checksums();
+    // DIRECT captures on the copy stream: it must also cover the checksum reads.
+    cuda_check(cudaStreamWaitEvent(copy_stream_, j->fnv_ev, 0), "wait checksums");
+  }
+  if (j->img == 0) {
+    mark_capture(pack_stream_);
+    return;
+  }
+  const uint32_t nsegs = static_cast<uint32_t>(j->segs.size());
+
+  if (mode == TS_D2H_RING) {
     const size_t nchunks = (j->img + chunk - 1) / chunk;
     j->chunk_events.assign(nchunks, nullptr);
     size_t w = 0;
@@ -668,6 +774,7 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       cuda_check(cudaEventRecord(packed, pack_stream_), "event");
       if (c + 1 == nchunks) mark_capture(pack_stream_);
       cuda_check(cudaStreamWaitEvent(copy_stream_, packed, 0), "wait pack");
+      if (nf && shadow) launch_checksums();  // reads the shadow, overlaps the D2H
       cudaEventDestroy(packed);  // destruction is deferred until the event completes
       for (; w < j->wins.size() && j->wins[w].lo < chi; ++w) {
         auto& win = j->wins[w];
@@ -743,6 +850,18 @@ void engine::completer_loop() {
       inflight_.pop_front();
     }
     auto& j = pw.j;
+    if (pw.fnv) {
+      const cudaError_t e = cudaEventSynchronize(j->fnv_ev);
+      put_event(j->fnv_ev);
+      j->fnv_ev = nullptr;
+      if (e != cudaSuccess) {
+        j->t->fail(TS_ERR_CUDA, std::string("checksum kernels failed: ") + cudaGetErrorString(e));
+        pool_->release(j->fnv_r);
+        continue;
+      }
+      fnv_landed(j);
+      continue;
+    }
     auto& win = j->wins[pw.w];
     const cudaError_t e = cudaEventSynchronize(win.ev);
     put_event(win.ev);
@@ -767,6 +886,7 @@ void engine::completer_loop() {
 
 void engine::window_landed(const std::shared_ptr<job>& j, size_t wi) {
   auto& w = j->wins[wi];
+  TRACE("landed rank=%d w=%zu pieces=%u fsegs=%u", j->rank_id, wi, w.wp_end - w.wp_begin, w.fs_end - w.fs_begin);
   uint8_t* base = pool_->data(w.r);
   for (uint32_t k = w.hp_begin; k < w.hp_end; ++k)
     std::memcpy(base + j->hp[k].win_off, j->hp[k].src, j->hp[k].len);  // host-tier bytes
@@ -774,9 +894,11 @@ void engine::window_landed(const std::shared_ptr<job>& j, size_t wi) {
   bool release_now = false;
   {
     std::lock_guard<std::mutex> g(j->mu);
-    w.refs = static_cast<int>(w.wp_end - w.wp_begin) + ((j->io && w.fs_end > w.fs_begin) ? 1 : 0);
+    w.refs = (j->io && w.fs_end > w.fs_begin) ? 1 : 0;
     for (uint32_t k = w.wp_begin; k < w.wp_end; ++k) {
       auto& r = j->raws[j->wp[k].obj];
+      if (j->gpu_ck && r.device) continue;  // checksummed on the device
+      w.refs += 1;
       r.q.push_back({base + j->wp[k].win_off, j->wp[k].len, static_cast<uint32_t>(wi)});
       if (!r.busy) {
         r.busy = true;
@@ -787,9 +909,29 @@ void engine::window_landed(const std::shared_ptr<job>& j, size_t wi) {
     release_now = w.refs == 0;
   }
   if (release_now) pool_->release(w.r);
-  for (uint32_t o : sched) workers_->submit([this, j, o] { hash_task(j, o); });
-  if (j->io && w.fs_end > w.fs_begin) workers_->submit([this, j, wi] { flush_window(j, wi); });
+  for (uint32_t o : sched) workers_->submit(guarded(j, [this, j, o] { hash_task(j, o); }));
+  if (j->io && w.fs_end > w.fs_begin) workers_->submit(guarded(j, [this, j, wi] { flush_window(j, wi); }));
   check_snapshot(j);
+}
+
+// Device checksums of every device-tier raw object landed (transfer.cpp:71-83's
+// per-object FNV, computed by the FNV kernels instead of the staging thread).
+void engine::fnv_landed(const std::shared_ptr<job>& j) {
+  const auto* res = reinterpret_cast<const uint64_t*>(pool_->data(j->fnv_r));
+  {
+    std::lock_guard<std::mutex> g(j->t->mu);
+    for (size_t i = 0; i < j->fnv_objs.size(); ++i) j->t->checksums[j->raws[j->fnv_objs[i]].oid] = res[i];
+  }
+  {
+    std::lock_guard<std::mutex> g(j->mu);
+    for (uint32_t k : j->fnv_objs) {
+      j->raws[k].hashed = j->raws[k].size;
+      j->files[j->raws[k].f].raw_pending -= 1;
+    }
+  }
+  pool_->release(j->fnv_r);
+  TRACE("checksums landed rank=%d objects=%zu", j->rank_id, j->fnv_objs.size());
+  for (size_t f = 0; f < j->files.size(); ++f) file_progress(j, f);
 }
 
 void engine::window_release_ref(const std::shared_ptr<job>& j, size_t wi) {
@@ -817,16 +959,15 @@ void engine::hash_task(const std::shared_ptr<job>& j, size_t oi) {
       r.q.pop_front();
     }
     r.fnv = fnv1a64(p.p, p.len, r.fnv);
-    bool done;
+    const bool done = r.hashed + p.len == r.size;
+    if (done) {  // publish the checksum before the file can see raw_pending == 0
+      std::lock_guard<std::mutex> g(j->t->mu);
+      j->t->checksums[r.oid] = r.fnv;
+    }
     {
       std::lock_guard<std::mutex> g(j->mu);
       r.hashed += p.len;
-      done = r.hashed == r.size;
       if (done) j->files[r.f].raw_pending -= 1;
-    }
-    if (done) {
-      std::lock_guard<std::mutex> g(j->t->mu);
-      j->t->checksums[r.oid] = r.fnv;
     }
     window_release_ref(j, p.w);
     if (done) file_progress(j, r.f);
@@ -871,6 +1012,7 @@ void engine::serialize_task(const std::shared_ptr<job>& j, size_t si) {
                static_cast<int64_t>(so.oid));
   }
   so.ck = fnv1a64(so.enc.data(), so.enc.size());
+  TRACE("serialized rank=%d oid=%llu bytes=%zu", j->rank_id, (unsigned long long)so.oid, so.enc.size());
   bool file_ready;
   {
     std::lock_guard<std::mutex> g(j->mu);
@@ -942,9 +1084,11 @@ void engine::file_progress(const std::shared_ptr<job>& j, size_t fi) {
   auto& f = j->files[fi];
   {
     std::lock_guard<std::mutex> g(j->mu);
+    TRACE("file_progress rank=%d f=%zu fin=%d enq=%d winp=%d rawp=%d app=%d landed=%zu/%zu", j->rank_id, fi,
+          (int)f.finalizing, (int)j->enqueue_done, f.win_pending, f.raw_pending, (int)f.appended, j->wins_landed,
+          j->wins.size());
     if (f.finalizing || !j->enqueue_done || f.win_pending != 0 || f.raw_pending != 0 || !f.appended)
       return;
-    if (j->wins_landed != j->wins.size()) return;
     f.finalizing = true;
   }
   {

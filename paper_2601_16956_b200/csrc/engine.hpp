@@ -138,6 +138,8 @@ class engine {
   void put_event(cudaEvent_t e);
   uint8_t* ensure_device_ring(uint64_t bytes);
   void* ensure_seg_buffer(uint64_t bytes);
+  uint8_t* ensure_fnv_buffer(uint64_t bytes);
+  void fnv_landed(const std::shared_ptr<job>& j);
 
   ts_engine_config cfg_;
   int rank_id_, device_, sms_;
@@ -148,6 +150,8 @@ class engine {
   uint64_t ring_bytes_ = 0;
   void* segbuf_ = nullptr;
   uint64_t segbuf_bytes_ = 0;
+  uint8_t* fnvbuf_ = nullptr;
+  uint64_t fnvbuf_bytes_ = 0;
 
   std::mutex ev_mu_;
   std::vector<cudaEvent_t> ev_free_;
@@ -158,6 +162,7 @@ class engine {
   struct pending_window {
     std::shared_ptr<job> j;
     size_t w;
+    bool fnv = false;  // device checksums of the job instead of a D2H window
   };
   std::deque<pending_window> inflight_;
   bool stopping_ = false, copier_done_ = false;

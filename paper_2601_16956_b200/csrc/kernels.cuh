@@ -56,6 +56,20 @@ void launch_pattern_verify(const pseg* d_segs, uint32_t nsegs, uint64_t total, u
                            uint64_t iteration, unsigned long long* d_mismatch, int ctas,
                            int threads, cudaStream_t st);
 
+// ---------------------------------------------------------------------------
+// Exact segment-parallel FNV-1a-64 (fnv.cu). Each object's state (in/out) is
+// chained: pass the seed for a fresh checksum, a previous state to continue.
+constexpr uint64_t kFnvSeg = 16384;
+struct fnv_obj {
+  const uint8_t* ptr;
+  uint64_t len;
+  uint64_t seg0;  // first global segment index (prefix sum of ceil(len / kFnvSeg))
+};
+inline uint64_t align_up_dev(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+uint64_t fnv_scratch_bytes(uint64_t nseg, uint32_t nobj);
+void launch_fnv(const fnv_obj* d_objs, uint32_t nobj, uint64_t nseg, uint64_t* d_states, void* d_scratch,
+                cudaStream_t st);
+
 int sm_count(int device);
 unsigned long long launches();
 void count_launch();

@@ -314,8 +314,8 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
       const uint64_t a = std::max(lo, p.pos), b = std::min(hi, p.pos + p.len);
       if (b <= a) continue;
       auto& o = objs[p.obj];
-      if (o.d->tier != TS_TIER_DEVICE)
-        std::memcpy(static_cast<uint8_t*>(const_cast<void*>(o.d->data)) + p.obj_off + (a - p.pos), hs + (a - lo), b - a);
+      if (o.d->tier == TS_TIER_DEVICE) continue;  // verified on the GPU after the scatter
+      std::memcpy(static_cast<uint8_t*>(const_cast<void*>(o.d->data)) + p.obj_off + (a - p.pos), hs + (a - lo), b - a);
       std::lock_guard<std::mutex> g(S.mu);
       S.slot_refs[slot] += 1;
       o.q.push_back({hs + (a - lo), {b - a, slot}});
@@ -335,7 +335,41 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
     });
   }
   cuda_check(cudaEventRecord(ev_b, st), "event");
+  // Device-tier objects: exact FNV kernels over the restored shards themselves
+  // (checks the whole chain file -> pinned -> H2D -> unpack).
+  std::vector<uint32_t> dev_objs;
+  for (uint32_t i = 0; i < objs.size(); ++i)
+    if (objs[i].d->tier == TS_TIER_DEVICE) dev_objs.push_back(i);
+  uint64_t* d_states = nullptr;
+  std::vector<uint64_t> dev_ck(dev_objs.size());
+  if (!dev_objs.empty() && S.err_status == TS_OK) {
+    std::vector<dev::fnv_obj> fo(dev_objs.size());
+    std::vector<uint64_t> seeds(dev_objs.size(), fnv_seed);
+    uint64_t nseg = 0;
+    for (size_t i = 0; i < dev_objs.size(); ++i) {
+      const auto& o = objs[dev_objs[i]];
+      fo[i] = {static_cast<const uint8_t*>(o.d->data), o.size, nseg};
+      nseg += (o.size + dev::kFnvSeg - 1) / dev::kFnvSeg;
+    }
+    const uint32_t nf = static_cast<uint32_t>(fo.size());
+    const uint64_t tb = align_up(nf * sizeof(dev::fnv_obj), 256), sb = align_up(nf * 8ull, 256);
+    uint8_t* fb = nullptr;
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&fb), tb + sb + dev::fnv_scratch_bytes(nseg, nf), st), "alloc");
+    cuda_check(cudaMemcpyAsync(fb, fo.data(), nf * sizeof(dev::fnv_obj), cudaMemcpyHostToDevice, st), "upload");
+    cuda_check(cudaMemcpyAsync(fb + tb, seeds.data(), nf * 8ull, cudaMemcpyHostToDevice, st), "upload");
+    dev::launch_fnv(reinterpret_cast<dev::fnv_obj*>(fb), nf, nseg, reinterpret_cast<uint64_t*>(fb + tb), fb + tb + sb, st);
+    launches += 6;
+    cuda_check(cudaGetLastError(), "checksum kernels");
+    cuda_check(cudaMemcpyAsync(dev_ck.data(), fb + tb, nf * 8ull, cudaMemcpyDeviceToHost, st), "download");
+    cuda_check(cudaFreeAsync(fb, st), "free");
+  }
   cuda_check(cudaStreamSynchronize(st), "restore stream");
+  for (size_t i = 0; i < dev_objs.size(); ++i) {
+    auto& o = objs[dev_objs[i]];
+    o.fnv = dev_ck[i];
+    o.hashed = o.size;
+  }
+  (void)d_states;
   float h2d_ms = 0;
   cudaEventElapsedTime(&h2d_ms, ev_a, ev_b);
   cudaEventDestroy(ev_a);

@@ -114,3 +114,31 @@ def test_kernel_launches_counted(gpu, native):
     arr = _descs(native, [(buf.data_ptr(), 1000, 1, 0)])
     native.call(native.lib.ts_pattern_fill, arr, 1, 1, 1, None)
     assert native.lib.ts_kernel_launch_count() == before + 1
+
+
+def test_fnv_device_matches_oracle(gpu, native, oracle):
+    """Segment-parallel FNV-1a kernels == the serial byte chain (common.hpp:44-51)
+    for every size class around the 16 KiB segment, misaligned starts, and chaining."""
+    from paper_2601_16956_b200 import api
+
+    rng = np.random.default_rng(8)
+    buf = torch.randint(0, 256, (12 << 20,), dtype=torch.uint8, device=gpu)
+    host = buf.cpu().numpy()
+    sizes = [0, 1, 2, 15, 16, 17, 255, 16383, 16384, 16385, 32768, 32769, 100_000, 3 << 20, 5 << 20]
+    sizes += [int(x) for x in rng.integers(1, 300_000, 40)]
+    views, exp = [], []
+    for s in sizes:
+        off = int(rng.integers(0, (12 << 20) - s - 1))
+        views.append(buf[off:off + s])
+        exp.append(oracle.fnv1a64(host[off:off + s]))
+    assert api.fnv1a64_device(views) == exp
+    # chaining: continue from the state after the first part
+    full = buf[7:7 + 1_000_003]
+    a, b = full[:400_001], full[400_001:]
+    ha = api.fnv1a64_device([a])[0]
+    assert api.fnv1a64_device([b], init=[ha]) == [oracle.fnv1a64(host[7:7 + 1_000_003])]
+    # all-zero and all-0xff inputs (degenerate low-byte trajectories)
+    z = torch.zeros(70_000, dtype=torch.uint8, device=gpu)
+    f = torch.full((70_000,), 255, dtype=torch.uint8, device=gpu)
+    assert api.fnv1a64_device([z, f]) == [oracle.fnv1a64(np.zeros(70_000, np.uint8)),
+                                           oracle.fnv1a64(np.full(70_000, 255, np.uint8))]

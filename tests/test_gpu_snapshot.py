@@ -40,6 +40,16 @@ def test_snapshot_bytes_equal_reference(gpu, tmp_path, name, mode):
         assert s["snapshot_done"] and s["persisted_done"] and not s["failed"]
 
 
+@pytest.mark.parametrize("name", ["hand_mixed", "zero3_tiny", "odd_layout"])
+@pytest.mark.parametrize("mode", MODES)
+def test_host_checksums_identical(gpu, tmp_path, name, mode):
+    """checksum_on_gpu=0 (host FNV threads over the pinned pool) writes the same bytes."""
+    rec = S.load_recipe(os.path.join(GOLDEN, "recipes", name + ".recipe"))
+    out = str(tmp_path / "ckpt")
+    checkpoint_recipe(rec, out, cfg_for(mode, checksum_on_gpu=False))
+    assert read_tree(out) == read_tree(os.path.join(GOLDEN, "trees", name))
+
+
 @pytest.mark.parametrize("strategy", ["sync", "two_phase", "lazy"])
 def test_strategies_identical(gpu, tmp_path, strategy):
     name = "hand_mixed"
