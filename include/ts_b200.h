@@ -167,6 +167,8 @@ typedef struct ts_engine_config {
   int32_t write_files;              /* 0 = snapshot-only run (no file I/O, bench only) */
   int32_t checksum_on_gpu;          /* 1 (default): exact segment-parallel FNV-1a kernels on the
                                        device copy; 0: host threads over the pinned pool */
+  int32_t flush_mmap;               /* 1 (default): fixed-region flushes copy into a shared mapping
+                                       of the file (parallel per file); 0: pwrite(2) */
 } ts_engine_config;
 
 void ts_engine_config_default(ts_engine_config* cfg);

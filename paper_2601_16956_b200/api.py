@@ -256,6 +256,7 @@ class EngineConfig:
     low_priority_stream: bool = True
     write_files: bool = True
     checksum_on_gpu: bool = True
+    flush_mmap: bool = True
 
     def to_c(self) -> N.EngineConfigC:
         c = N.EngineConfigC()
@@ -277,6 +278,7 @@ class EngineConfig:
         c.low_priority_stream = int(self.low_priority_stream)
         c.write_files = int(self.write_files)
         c.checksum_on_gpu = int(self.checksum_on_gpu)
+        c.flush_mmap = int(self.flush_mmap)
         return c
 
 

@@ -194,6 +194,7 @@ void ts_engine_config_default(ts_engine_config* c) {
   c->low_priority_stream = 1;
   c->write_files = 1;
   c->checksum_on_gpu = 1;
+  c->flush_mmap = 1;
 }
 
 ts_status ts_engine_create(const ts_engine_config* cfg, int rank_id, int device, ts_engine** out) {

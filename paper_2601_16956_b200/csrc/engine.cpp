@@ -270,6 +270,10 @@ struct job {
   bool io = true;
   // device checksums (checksum_on_gpu): device-tier raw objects hashed by the
   // FNV kernels; results land in a pool region
+  // D2H order of the windows when the whole image is addressable (shadow,
+  // direct, zero-copy): files interleaved in proportion to their size, so the
+  // flushers fill every file concurrently from the first window on.
+  std::vector<uint32_t> worder;
   bool gpu_ck = false;
   std::vector<uint32_t> fnv_objs;
   pinned_pool::region fnv_r;
@@ -459,6 +463,7 @@ std::shared_ptr<ticket_state> engine::issue(session& s, const ts_rank_info& rank
                                          fp.tensor_region_end, j->plan.hash, cfg_.overwrite != 0,
                                          j->io);
     fs.append_end = fp.tensor_region_end;
+    if (cfg_.flush_mmap) fs.w->map_fixed_region();
     fidx.emplace(fp.file_id, static_cast<uint32_t>(j->files.size()));
     j->files.push_back(std::move(fs));
   }
@@ -535,6 +540,20 @@ std::shared_ptr<ticket_state> engine::issue(session& s, const ts_rank_info& rank
       w.hp_end = static_cast<uint32_t>(j->hp.size());
       j->wins.push_back(w);
     }
+    std::vector<std::pair<double, uint32_t>> key(j->wins.size());
+    for (size_t k = 0; k < j->wins.size(); ++k) {
+      const auto& w = j->wins[k];
+      double frac = 0;
+      if (w.fs_end > w.fs_begin) {
+        const auto& f = j->files[j->fs[w.fs_begin].f];
+        frac = double(w.lo > f.img ? w.lo - f.img : 0) / double(std::max<uint64_t>(1, f.tre - header_reserved));
+      }
+      key[k] = {frac, static_cast<uint32_t>(k)};
+    }
+    // Host-hashed pieces must reach their checksum actor in object order.
+    const bool host_hashed = !cfg_.checksum_on_gpu || !j->hp.empty();
+    if (!host_hashed) std::stable_sort(key.begin(), key.end());
+    for (const auto& kv : key) j->worder.push_back(kv.second);
   }
 
   // Structured objects, in rank.objects order (the canonical append order).
@@ -776,14 +795,14 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       cuda_check(cudaStreamWaitEvent(copy_stream_, packed, 0), "wait pack");
       if (nf && shadow) launch_checksums();  // reads the shadow, overlaps the D2H
       cudaEventDestroy(packed);  // destruction is deferred until the event completes
-      for (; w < j->wins.size() && j->wins[w].lo < chi; ++w) {
-        auto& win = j->wins[w];
+      for (size_t q = w; q < j->wins.size() && j->wins[q].lo < chi; ++q, ++w) {
+        auto& win = j->wins[shadow ? j->worder[q] : q];
         acquire(win);
         cuda_check(cudaMemcpyAsync(pool_->data(win.r), slot + (win.lo - clo), win.hi - win.lo,
                                    cudaMemcpyDeviceToHost, copy_stream_), "D2H window");
         t.copies += 1;
         cuda_check(cudaEventRecord(win.ev, copy_stream_), "event");
-        push_window(w);
+        push_window(shadow ? j->worder[q] : q);
         if (failed()) break;
       }
       cudaEvent_t done;
@@ -797,7 +816,8 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dbase), pool_->base(), 0),
                "cudaHostGetDevicePointer");
     cuda_check(cudaEventRecord(t.ev_d2h_first, pack_stream_), "event");
-    for (size_t w = 0; w < j->wins.size() && !failed(); ++w) {
+    for (size_t q = 0; q < j->wins.size() && !failed(); ++q) {
+      const size_t w = j->worder[q];
       auto& win = j->wins[w];
       acquire(win);
       dev::launch_pack(d_segs, nsegs, win.lo, win.hi, dbase + win.r.offset, ctas, threads, pack_stream_);
@@ -810,14 +830,16 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     mark_capture(pack_stream_);
   } else {  // DIRECT: copy-engine DMA per fragment piece, gaps zeroed on the host
     cuda_check(cudaEventRecord(t.ev_d2h_first, copy_stream_), "event");
-    size_t k = 0;
-    for (size_t w = 0; w < j->wins.size() && !failed(); ++w) {
+    for (size_t q = 0; q < j->wins.size() && !failed(); ++q) {
+      const size_t w = j->worder[q];
       auto& win = j->wins[w];
       acquire(win);
       uint8_t* dst = pool_->data(win.r);
-      while (k < j->segs.size() && j->segs[k].pos + j->segs[k].len <= win.lo) ++k;
-      for (size_t q = k; q < j->segs.size() && j->segs[q].pos < win.hi; ++q) {
-        const auto& sg = j->segs[q];
+      size_t k = std::upper_bound(j->segs.begin(), j->segs.end(), win.lo,
+                                  [](uint64_t x, const dev::seg& sg) { return x < sg.pos; }) - j->segs.begin();
+      k = k ? k - 1 : 0;
+      for (size_t qq = k; qq < j->segs.size() && j->segs[qq].pos < win.hi; ++qq) {
+        const auto& sg = j->segs[qq];
         const uint64_t a = std::max(win.lo, sg.pos), b = std::min(win.hi, sg.pos + sg.len);
         if (b <= a) continue;
         if (sg.src) {
@@ -986,7 +1008,7 @@ void engine::flush_window(const std::shared_ptr<job>& j, size_t wi) {
     try {
       for (uint32_t k = w.fs_begin; k < w.fs_end; ++k) {
         const auto& s = j->fs[k];
-        j->files[s.f].w->write_at(s.file_off, base + s.win_off, s.len);
+        j->files[s.f].w->write_fixed(s.file_off, base + s.win_off, s.len);
       }
     } catch (const error& e) {
       j->t->fail(e.status, std::string("flush failed: ") + e.what(), e.object_id);

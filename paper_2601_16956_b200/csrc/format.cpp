@@ -2,7 +2,9 @@
 #include "format.hpp"
 
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <sys/stat.h>
+#include <sys/statvfs.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -171,7 +173,26 @@ file_writer::file_writer(const std::string& path, uint64_t tre, uint64_t plan_ha
 }
 
 file_writer::~file_writer() {
+  if (map_) ::munmap(map_, tre_);
   if (fd_ >= 0) ::close(fd_);
+}
+
+void file_writer::map_fixed_region() {
+  if (!io_ || map_ || tre_ <= header_reserved) return;
+  // A fault on a full filesystem raises SIGBUS instead of returning ENOSPC:
+  // only map when the space is there, else keep positional writes.
+  struct statvfs vs;
+  if (::fstatvfs(fd_, &vs) != 0 || static_cast<uint64_t>(vs.f_bavail) * vs.f_frsize < tre_ + (64ull << 20)) return;
+  void* m = ::mmap(nullptr, tre_, PROT_READ | PROT_WRITE, MAP_SHARED, fd_, 0);
+  if (m == MAP_FAILED) return;  // fall back to positional writes
+  map_ = static_cast<uint8_t*>(m);
+}
+
+void file_writer::write_fixed(uint64_t off, const void* p, size_t n) {
+  if (!io_ || n == 0) return;
+  if (off < header_reserved || off + n > tre_) fail(TS_ERR_IO, "fixed write outside the tensor region");
+  if (map_) std::memcpy(map_ + off, p, n);
+  else pwrite_all(fd_, static_cast<const uint8_t*>(p), n, off, path_);
 }
 
 void file_writer::write_at(uint64_t off, const void* p, size_t n) {
@@ -182,6 +203,10 @@ void file_writer::write_at(uint64_t off, const void* p, size_t n) {
 void file_writer::finalize_at(uint64_t off, const std::vector<footer_entry>& entries) {
   validate_entries(entries, tre_);
   if (!io_) return;
+  if (map_) {
+    ::munmap(map_, tre_);
+    map_ = nullptr;
+  }
   const auto blob = footer_blob(entries);
   pwrite_all(fd_, blob.data(), blob.size(), off, path_);
 }

@@ -55,6 +55,12 @@ class file_writer {
               bool overwrite, bool io);
   ~file_writer();
   void write_at(uint64_t off, const void* p, size_t n);
+  // Fixed-region writes through a shared mapping of [0, tensor_region_end):
+  // a page-cache file accepts one writer at a time through write(2) (the inode
+  // lock), but page faults and copies into a shared mapping proceed in
+  // parallel, so many flush threads can fill one file concurrently.
+  void map_fixed_region();
+  void write_fixed(uint64_t off, const void* p, size_t n);
   void finalize_at(uint64_t off, const std::vector<footer_entry>& entries);
   const std::string& path() const { return path_; }
 
@@ -63,6 +69,7 @@ class file_writer {
   int fd_ = -1;
   uint64_t tre_;
   bool io_;
+  uint8_t* map_ = nullptr;
 };
 
 struct file_header {
