@@ -40,17 +40,16 @@ class Value:
     """Owning handle of a native TLV value."""
 
     __slots__ = ("h",)
-    _free = N.lib.ts_value_free
 
     def __init__(self, h: int):
         if not h:
             raise TsError(N.ERR_GENERIC, "null value handle")
         self.h = h
 
-    def __del__(self):
+    def __del__(self, _free=N.lib.ts_value_free):
         h, self.h = getattr(self, "h", None), None
         if h:
-            Value._free(h)
+            _free(h)
 
     @staticmethod
     def from_py(v: Any) -> "Value":
@@ -345,13 +344,13 @@ class TransferTicket:
         self.h = h
         self._keep = keep  # structured values the serializers still read
 
-    def __del__(self):
+    def __del__(self, _wait=N.lib.ts_ticket_wait_snapshot, _rel=N.lib.ts_ticket_release):
         h, self.h = getattr(self, "h", None), None
         if h:
             try:
-                N.lib.ts_ticket_wait_snapshot(h, None)  # serializers hold raw pointers to _keep
+                _wait(h, None)  # serializers hold raw pointers to _keep
             finally:
-                N.lib.ts_ticket_release(h)
+                _rel(h)
 
     def _wait(self, fn) -> int:
         ns = C.c_int64()
@@ -568,10 +567,10 @@ class Restorer:
         self.h = h.value
         self.last_stats: Dict[str, Any] = {}
 
-    def __del__(self):
+    def __del__(self, _close=N.lib.ts_restore_close):
         h, self.h = getattr(self, "h", None), None
         if h:
-            N.lib.ts_restore_close(h)
+            _close(h)
 
     @property
     def n_ranks(self) -> int:

@@ -931,6 +931,13 @@ void engine::window_landed(const std::shared_ptr<job>& j, size_t wi) {
     release_now = w.refs == 0;
   }
   if (release_now) pool_->release(w.r);
+  bool last;
+  {
+    std::lock_guard<std::mutex> g(j->mu);
+    last = j->wins_landed == j->wins.size();
+  }
+  if (last)
+    for (size_t f = 0; f < j->files.size(); ++f) file_progress(j, f);
   for (uint32_t o : sched) workers_->submit(guarded(j, [this, j, o] { hash_task(j, o); }));
   if (j->io && w.fs_end > w.fs_begin) workers_->submit(guarded(j, [this, j, wi] { flush_window(j, wi); }));
   check_snapshot(j);
@@ -1111,6 +1118,7 @@ void engine::file_progress(const std::shared_ptr<job>& j, size_t fi) {
           j->wins.size());
     if (f.finalizing || !j->enqueue_done || f.win_pending != 0 || f.raw_pending != 0 || !f.appended)
       return;
+    if (j->wins_landed != j->wins.size()) return;  // persisted implies staged
     f.finalizing = true;
   }
   {
