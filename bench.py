@@ -202,24 +202,37 @@ def ours(args):
     img_est = raw + 4096 * (len(spec.objects) + 4)
     free, _ = torch.cuda.mem_get_info(local)
     shadow = img_est + (256 << 20) <= free - (24 << 30)  # keep room for the GEMM load
-    pool = (img_est + (64 << 20) + (2 << 20) - 1) // (2 << 20) * (2 << 20)
+    # pinned pool: the whole image when host RAM allows (one pinning at engine
+    # creation), else a bounded pool with back-pressure (staging.cpp semantics)
+    pool_cap = int(args.pool_gb * (1 << 30)) if args.pool_gb else 64 << 30
+    pool = (min(img_est + (64 << 20), pool_cap) + (2 << 20) - 1) // (2 << 20) * (2 << 20)
     cfg = api.EngineConfig(d2h_mode=args.mode, staging_capacity_bytes=pool, raw_chunk_bytes=64 << 20,
-                           device_staging_bytes=img_est + (1 << 20) if shadow else 8 << 30,
+                           device_staging_bytes=img_est + (1 << 20) if shadow else int(args.ring_gb * (1 << 30)),
                            flush_workers=min(16, os.cpu_count() or 8), write_files=False)
     eng = api.CheckpointEngine(cfg, spec.rank_id, local)
-    echo = None
-    tdir = tempfile.mkdtemp(dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
+    full = getattr(rec, "full_layout", None)
+    echo = S.Recipe(layout=full).manifest_echo() if full else rec.manifest_echo()
+    tdir = os.path.join("/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir(), "ts_bench")
+    if rank == 0:
+        shutil.rmtree(tdir, ignore_errors=True)
+        os.makedirs(tdir, exist_ok=True)
+    if ws > 1:
+        dist.barrier()
     launches0 = api.N.lib.ts_kernel_launch_count()
 
     def step(it, engine, write):
         api.mutate_update_step(state, it)
-        sess = api.CheckpointSession(os.path.join(tdir, f"ckpt_{it:06d}") if write else "", it, it, echo, 1,
-                                     writes_manifest=write)
+        sess = api.CheckpointSession(os.path.join(tdir, f"ckpt_{it:06d}") if write else "", it, it, echo,
+                                     ws if write else 1, writes_manifest=write and rank == 0)
         t = engine.issue_checkpoint(sess, state, it)
         t.wait_snapshot()
         t.wait_persisted()
         if write:
-            sess.wait_complete(600)
+            if ws > 1:  # the only collective: allgather of manifest blobs, rank 0 commits
+                from paper_2601_16956_b200 import distributed as D
+                D.commit_manifest(sess, [spec.rank_id])
+            else:
+                sess.wait_complete(600)
         st = t.stats()
         return st, sess
 
@@ -274,9 +287,8 @@ def ours(args):
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
-        for _ in range(args.e2e_steps):
+        for _ in range(args.e2e_steps):  # checkpoints are deleted after the timed region
             it += 1
-            shutil.rmtree(os.path.join(tdir, f"ckpt_{it - 2:06d}"), ignore_errors=True)
             st, sess = step(it, eng_io, True)
         f1.record()
         torch.cuda.synchronize()
@@ -291,11 +303,12 @@ def ours(args):
         # restore of the last checkpoint (H2D + scatter-unpack + FNV verify)
         man = os.path.join(tdir, f"ckpt_{it:06d}", "MANIFEST.tlv")
         r = api.Restorer(man)
-        rs = r.restore_rank(0, local)
+        ridx = [r.rank_info(i).rank_id for i in range(r.n_ranks)].index(spec.rank_id)
+        rs = r.restore_rank(ridx, local)
         torch.cuda.synchronize()
         t0 = time.time()
         r2 = api.Restorer(man)
-        r2.restore_rank(0, local, into=rs)
+        r2.restore_rank(ridx, local, into=rs)
         torch.cuda.synchronize()
         restore_s = time.time() - t0
         for o, so in zip(rs.objects, spec.objects):
@@ -309,7 +322,10 @@ def ours(args):
         eng_io.shutdown()
     else:
         eng.shutdown()
-    shutil.rmtree(tdir, ignore_errors=True)
+    if ws > 1:
+        dist.barrier()
+    if rank == 0:
+        shutil.rmtree(tdir, ignore_errors=True)
 
     # --- training-blocked time with a synthetic fwd/bwd load ------------------
     blocked = None
@@ -331,7 +347,7 @@ def ours(args):
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": f"{args.config}: {rec.name} rank-r shard, {len(spec.objects)} objects, "
                                    f"{bytes_step / 1e9:.3f} GB/rank", "d2h_mode": args.mode,
-                       "device_shadow": bool(shadow), "l2": "inputs > L2 (126 MB)",
+                       "device_shadow": bool(shadow), "pinned_pool_gb": round(pool / 2**30, 2), "l2": "inputs > L2 (126 MB)",
                        "step": "update(pattern kernel) + issue + snapshot + checksums (no files)"},
             "per_gpu_gbps": round(value / ws, 3),
             "snapshot_ms_mean": round(statistics.mean(snap_ms), 2),
@@ -407,6 +423,8 @@ def main():
     ap.add_argument("--train-steps", type=int, default=3)
     ap.add_argument("--fwd-bwd-ms", type=float, default=1800.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pool-gb", type=float, default=0.0, help="pinned pool cap (default: image, at most 64 GiB)")
+    ap.add_argument("--ring-gb", type=float, default=8.0, help="HBM staging ring when no full device shadow fits")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)

@@ -554,18 +554,19 @@ ts_status ts_fnv1a64_device(const void* const* ptrs, const uint64_t* sizes, size
     auto st = static_cast<cudaStream_t>(stream);
     std::vector<dev::fnv_obj> objs(n);
     std::vector<uint64_t> states(n);
-    uint64_t nseg = 0;
     for (size_t i = 0; i < n; ++i) {
-      objs[i] = {static_cast<const uint8_t*>(ptrs[i]), sizes[i], nseg};
-      nseg += (sizes[i] + dev::kFnvSeg - 1) / dev::kFnvSeg;
+      objs[i] = {static_cast<const uint8_t*>(ptrs[i]), sizes[i], 0, 0};
       states[i] = init ? init[i] : fnv_seed;
     }
+    uint64_t nchunk = 0;
+    const uint64_t nseg = dev::fnv_prepare(objs.data(), static_cast<uint32_t>(n), &nchunk);
     const uint64_t tb = dev::align_up_dev(n * sizeof(dev::fnv_obj), 256), sb = dev::align_up_dev(n * 8, 256);
     uint8_t* buf = nullptr;
-    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&buf), tb + sb + dev::fnv_scratch_bytes(nseg, static_cast<uint32_t>(n)), st), "alloc");
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&buf),
+                               tb + sb + dev::fnv_scratch_bytes(nseg, nchunk, static_cast<uint32_t>(n)), st), "alloc");
     cuda_check(cudaMemcpyAsync(buf, objs.data(), n * sizeof(dev::fnv_obj), cudaMemcpyHostToDevice, st), "upload");
     cuda_check(cudaMemcpyAsync(buf + tb, states.data(), n * 8, cudaMemcpyHostToDevice, st), "upload");
-    dev::launch_fnv(reinterpret_cast<dev::fnv_obj*>(buf), static_cast<uint32_t>(n), nseg,
+    dev::launch_fnv(reinterpret_cast<dev::fnv_obj*>(buf), static_cast<uint32_t>(n), nseg, nchunk,
                     reinterpret_cast<uint64_t*>(buf + tb), buf + tb + sb, st);
     cuda_check(cudaGetLastError(), "fnv launch");
     cuda_check(cudaMemcpyAsync(out, buf + tb, n * 8, cudaMemcpyDeviceToHost, st), "download");

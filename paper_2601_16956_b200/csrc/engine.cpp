@@ -729,18 +729,18 @@ void engine::run_job(const std::shared_ptr<job>& j) {
   // path), else over the state itself before the capture completes.
   const uint32_t nf = static_cast<uint32_t>(j->fnv_objs.size());
   uint8_t* fbuf = nullptr;
-  uint64_t fnseg = 0, ftb = 0, fsb = 0;
+  uint64_t fnseg = 0, fnchunk = 0, ftb = 0, fsb = 0;
   if (nf) {
     std::vector<dev::fnv_obj> fo(nf);
     std::vector<uint64_t> st(nf, fnv_seed);
     for (uint32_t i = 0; i < nf; ++i) {
       const auto& r = j->raws[j->fnv_objs[i]];
-      fo[i] = {shadow ? ring + r.img : r.src, r.size, fnseg};
-      fnseg += (r.size + dev::kFnvSeg - 1) / dev::kFnvSeg;
+      fo[i] = {shadow ? ring + r.img : r.src, r.size, 0, 0};
     }
+    fnseg = dev::fnv_prepare(fo.data(), nf, &fnchunk);
     ftb = align_up(nf * sizeof(dev::fnv_obj), 256);
     fsb = align_up(nf * 8ull, 256);
-    fbuf = ensure_fnv_buffer(ftb + fsb + dev::fnv_scratch_bytes(fnseg, nf));
+    fbuf = ensure_fnv_buffer(ftb + fsb + dev::fnv_scratch_bytes(fnseg, fnchunk, nf));
     cuda_check(cudaMemcpyAsync(fbuf, fo.data(), nf * sizeof(dev::fnv_obj), cudaMemcpyHostToDevice, pack_stream_),
                "upload checksum table");
     cuda_check(cudaMemcpyAsync(fbuf + ftb, st.data(), nf * 8ull, cudaMemcpyHostToDevice, pack_stream_),
@@ -749,12 +749,15 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     j->fnv_ev = get_event();
   }
   auto launch_checksums = [&] {
-    dev::launch_fnv(reinterpret_cast<dev::fnv_obj*>(fbuf), nf, fnseg, reinterpret_cast<uint64_t*>(fbuf + ftb),
-                    fbuf + ftb + fsb, pack_stream_);
-    t.kernel_launches += 6;
+    // Results are stored by the last kernel straight into the mapped pool region:
+    // a cudaMemcpy would queue behind the bulk D2H windows on the copy engine.
+    uint64_t* out = nullptr;
+    cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&out), pool_->data(j->fnv_r), 0),
+               "cudaHostGetDevicePointer");
+    dev::launch_fnv(reinterpret_cast<dev::fnv_obj*>(fbuf), nf, fnseg, fnchunk,
+                    reinterpret_cast<uint64_t*>(fbuf + ftb), fbuf + ftb + fsb, pack_stream_, out);
+    t.kernel_launches += 11;
     cuda_check(cudaGetLastError(), "checksum kernels");
-    cuda_check(cudaMemcpyAsync(pool_->data(j->fnv_r), fbuf + ftb, nf * 8ull, cudaMemcpyDeviceToHost, pack_stream_),
-               "checksums D2H");
     cuda_check(cudaEventRecord(j->fnv_ev, pack_stream_), "event");
     {
       std::lock_guard<std::mutex> g(mu_);
@@ -1098,6 +1101,7 @@ void engine::check_snapshot(const std::shared_ptr<job>& j) {
     {
       std::lock_guard<std::mutex> g(j->t->mu);
       if (!j->t->failed && j->wins_landed == j->wins.size()) {
+        TRACE("snapshot rank=%d", j->rank_id);
         j->t->snapshot = true;
         j->t->t_snapshot = now_ns() - j->t->t_issue;
         cudaEventElapsedTime(&j->t->d2h_ms, j->t->ev_d2h_first, j->t->ev_d2h_last);

@@ -140,34 +140,85 @@ __global__ void __launch_bounds__(256) fnv_pass_c(const fnv_obj* __restrict__ o,
   cseg[g] = c & kM56;
 }
 
-// Serial scans over each object's segments (one thread per object).
-__global__ void fnv_scan_a(const fnv_obj* __restrict__ o, uint32_t n, const uint64_t* __restrict__ states,
-                           const uint64_t* __restrict__ piA, uint8_t* __restrict__ lo_start,
-                           uint8_t* __restrict__ lo_end) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint64_t g0 = o[i].seg0, g1 = g0 + (o[i].len + kFnvSeg - 1) / kFnvSeg;
-  uint32_t lo = static_cast<uint32_t>(states[i] & 15);
-  for (uint64_t g = g0; g < g1; ++g) {
-    lo_start[g] = static_cast<uint8_t>(lo);
-    lo = static_cast<uint32_t>(piA[g] >> (4 * lo)) & 15u;
-  }
-  lo_end[i] = static_cast<uint8_t>(lo);
+// ---------------------------------------------------------------------------
+// Scans over each object's segments. The per-segment maps (nibble maps for
+// passes A/B, affine maps H -> a*H + c for the combine) compose associatively,
+// so each object's chain is cut into chunks of kChunk segments: compose each
+// chunk in parallel, run the short serial chain over chunks, then expand the
+// chunk starts back to segment starts in parallel.
+
+constexpr uint32_t kChunk = 64;
+
+__device__ __forceinline__ uint32_t nib(uint64_t m, uint32_t i) { return static_cast<uint32_t>(m >> (4 * i)) & 15u; }
+
+// (m after p): x -> m[p[x]]
+__device__ __forceinline__ uint64_t nib_compose(uint64_t m, uint64_t p) {
+  uint64_t r = 0;
+#pragma unroll
+  for (uint32_t x = 0; x < 16; ++x) r |= static_cast<uint64_t>(nib(m, nib(p, x))) << (4 * x);
+  return r;
 }
 
-__global__ void fnv_scan_b(const fnv_obj* __restrict__ o, uint32_t n, const uint64_t* __restrict__ states,
-                           const uint64_t* __restrict__ piB, uint8_t* __restrict__ start,
-                           uint8_t* __restrict__ lend) {
+__device__ __forceinline__ uint64_t obj_nseg(const fnv_obj& o) { return (o.len + kFnvSeg - 1) / kFnvSeg; }
+
+// chunk c of the global chunk space -> (object, first segment, segment count)
+struct chunk_ref {
+  uint32_t obj;
+  uint64_t g0, n;
+};
+__device__ __forceinline__ chunk_ref chunk_of(const fnv_obj* __restrict__ o, uint32_t n, uint64_t c) {
+  uint32_t lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(&o[mid].chunk0) <= c) lo = mid;
+    else hi = mid;
+  }
+  const uint64_t k = c - o[lo].chunk0;
+  const uint64_t ns = obj_nseg(o[lo]);
+  const uint64_t g0 = o[lo].seg0 + k * kChunk;
+  return {lo, g0, umin64(kChunk, ns - k * kChunk)};
+}
+
+__global__ void fnv_chunk_nib(const fnv_obj* __restrict__ o, uint32_t n,
+                              uint64_t nchunk, const uint64_t* __restrict__ pi, uint64_t* __restrict__ cpi) {
+  const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= nchunk) return;
+  const chunk_ref r = chunk_of(o, n, c);
+  uint64_t m = 0xfedcba9876543210ull;
+  for (uint64_t s = 0; s < r.n; ++s) m = nib_compose(pi[r.g0 + s], m);
+  cpi[c] = m;
+}
+
+// Serial chain over an object's chunks: start nibble of every chunk.
+// `shift` selects the nibble of the state the chain starts from (0: low, 4: high).
+__global__ void fnv_chain_nib(const fnv_obj* __restrict__ o, uint32_t n,
+                              const uint64_t* __restrict__ states, const uint64_t* __restrict__ cpi,
+                              uint8_t* __restrict__ cstart, uint8_t* __restrict__ end_nib, uint32_t shift) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const uint64_t g0 = o[i].seg0, g1 = g0 + (o[i].len + kFnvSeg - 1) / kFnvSeg;
-  uint32_t hi = static_cast<uint32_t>(states[i] >> 4) & 15u;
-  for (uint64_t g = g0; g < g1; ++g) {
-    const uint32_t lo = start[g];  // holds lo_start on entry
-    start[g] = static_cast<uint8_t>((hi << 4) | lo);
-    hi = static_cast<uint32_t>(piB[g] >> (4 * hi)) & 15u;
+  const uint64_t c0 = o[i].chunk0, c1 = c0 + (obj_nseg(o[i]) + kChunk - 1) / kChunk;
+  uint32_t x = static_cast<uint32_t>(states[i] >> shift) & 15u;
+  for (uint64_t c = c0; c < c1; ++c) {
+    cstart[c] = static_cast<uint8_t>(x);
+    x = nib(cpi[c], x);
   }
-  lend[i] = static_cast<uint8_t>((hi << 4) | lend[i]);
+  end_nib[i] = static_cast<uint8_t>(x);
+}
+
+// Expand chunk starts to segment starts. mode 0: out[g] = lo nibble;
+// mode 1: out[g] = (hi << 4) | out[g] (out holds the low nibbles on entry).
+__global__ void fnv_expand_nib(const fnv_obj* __restrict__ o, uint32_t n,
+                               uint64_t nchunk, const uint64_t* __restrict__ pi,
+                               const uint8_t* __restrict__ cstart, uint8_t* __restrict__ out, int mode) {
+  const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= nchunk) return;
+  const chunk_ref r = chunk_of(o, n, c);
+  uint32_t x = cstart[c];
+  for (uint64_t s = 0; s < r.n; ++s) {
+    const uint64_t g = r.g0 + s;
+    out[g] = static_cast<uint8_t>(mode == 0 ? x : ((x << 4) | out[g]));
+    x = nib(pi[g], x);
+  }
 }
 
 __device__ __forceinline__ uint64_t pow_p(uint64_t k) {
@@ -180,56 +231,104 @@ __device__ __forceinline__ uint64_t pow_p(uint64_t k) {
   return r;
 }
 
-__global__ void fnv_combine(const fnv_obj* __restrict__ o, uint32_t n, uint64_t* __restrict__ states,
-                            const uint64_t* __restrict__ cseg, const uint8_t* __restrict__ lend) {
+// Affine composition over a chunk: H -> a*H + c (mod 2^56).
+__global__ void fnv_chunk_affine(const fnv_obj* __restrict__ o, uint32_t n,
+                                 uint64_t nchunk, const uint64_t* __restrict__ cseg, uint64_t* __restrict__ ca,
+                                 uint64_t* __restrict__ cc) {
+  const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= nchunk) return;
+  const chunk_ref r = chunk_of(o, n, c);
+  const uint64_t pk = pow_p(kFnvSeg);
+  uint64_t a = 1, cv = 0;
+  const fnv_obj& ob = o[r.obj];
+  for (uint64_t s = 0; s < r.n; ++s) {
+    const uint64_t g = r.g0 + s;
+    const uint64_t len = umin64(kFnvSeg, ob.len - (g - ob.seg0) * kFnvSeg);
+    const uint64_t m = len == kFnvSeg ? pk : pow_p(len);
+    a = (m * a) & kM56;
+    cv = (m * cv + cseg[g]) & kM56;
+  }
+  ca[c] = a;
+  cc[c] = cv;
+}
+
+__global__ void fnv_combine(const fnv_obj* __restrict__ o, uint32_t n,
+                            uint64_t* __restrict__ states, const uint64_t* __restrict__ ca,
+                            const uint64_t* __restrict__ cc, const uint8_t* __restrict__ lo_end,
+                            const uint8_t* __restrict__ hi_end, uint64_t* __restrict__ out) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  if (o[i].len == 0) return;
-  const uint64_t nseg = (o[i].len + kFnvSeg - 1) / kFnvSeg;
-  const uint64_t pk = pow_p(kFnvSeg);
-  uint64_t H = states[i] >> 8;
-  for (uint64_t s = 0; s < nseg; ++s) {
-    const uint64_t len = umin64(kFnvSeg, o[i].len - s * kFnvSeg);
-    const uint64_t m = len == kFnvSeg ? pk : pow_p(len);
-    H = (m * H + cseg[o[i].seg0 + s]) & kM56;
+  if (o[i].len == 0) {
+    if (out) out[i] = states[i];
+    return;
   }
-  states[i] = (H << 8) | lend[i];
+  const uint64_t c0 = o[i].chunk0, c1 = c0 + (obj_nseg(o[i]) + kChunk - 1) / kChunk;
+  uint64_t H = states[i] >> 8;
+  for (uint64_t c = c0; c < c1; ++c) H = (ca[c] * H + cc[c]) & kM56;
+  const uint64_t h = (H << 8) | (static_cast<uint64_t>(hi_end[i]) << 4) | lo_end[i];
+  states[i] = h;
+  if (out) out[i] = h;  // mapped pinned memory: no copy-engine round trip behind bulk D2H
 }
 
 }  // namespace
 
-uint64_t fnv_scratch_bytes(uint64_t nseg, uint32_t nobj) {
-  return align_up_dev(nseg * 8, 256) * 2 + align_up_dev(nseg, 256) + align_up_dev(nobj, 256);
+uint64_t fnv_scratch_bytes(uint64_t nseg, uint64_t nchunk, uint32_t nobj) {
+  return align_up_dev(nseg * 8, 256) * 2 + align_up_dev(nseg, 256) + align_up_dev(nchunk * 8, 256) * 3 +
+         align_up_dev(nchunk, 256) + align_up_dev(nobj, 256) * 2;
 }
 
-void launch_fnv(const fnv_obj* d_objs, uint32_t nobj, uint64_t nseg, uint64_t* d_states, void* d_scratch,
-                cudaStream_t st) {
+uint64_t fnv_prepare(fnv_obj* objs, uint32_t n, uint64_t* nchunk) {
+  uint64_t g = 0, c = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint64_t ns = (objs[i].len + kFnvSeg - 1) / kFnvSeg;
+    objs[i].seg0 = g;
+    objs[i].chunk0 = c;
+    g += ns;
+    c += (ns + kChunk - 1) / kChunk;
+  }
+  *nchunk = c;
+  return g;
+}
+
+void launch_fnv(const fnv_obj* d_objs, uint32_t nobj, uint64_t nseg, uint64_t nchunk, uint64_t* d_states,
+                void* d_scratch, cudaStream_t st, uint64_t* out_mapped) {
   if (nobj == 0) return;
   uint8_t* s = static_cast<uint8_t*>(d_scratch);
-  uint64_t* a = reinterpret_cast<uint64_t*>(s);  // piA, reused for C
-  uint64_t* b = reinterpret_cast<uint64_t*>(s + align_up_dev(nseg * 8, 256));
-  uint8_t* lst = s + 2 * align_up_dev(nseg * 8, 256);
-  uint8_t* lend = lst + align_up_dev(nseg, 256);
+  auto take = [&](uint64_t bytes) {
+    uint8_t* p = s;
+    s += align_up_dev(bytes, 256);
+    return p;
+  };
+  uint64_t* pa = reinterpret_cast<uint64_t*>(take(nseg * 8));  // piA, later C_seg
+  uint64_t* pb = reinterpret_cast<uint64_t*>(take(nseg * 8));  // piB
+  uint8_t* lst = take(nseg);                                   // segment start nibble, then byte
+  uint64_t* cpi = reinterpret_cast<uint64_t*>(take(nchunk * 8));
+  uint64_t* ca = reinterpret_cast<uint64_t*>(take(nchunk * 8));
+  uint64_t* cc = reinterpret_cast<uint64_t*>(take(nchunk * 8));
+  uint8_t* cst = take(nchunk);
+  uint8_t* lo_end = take(nobj);
+  uint8_t* hi_end = take(nobj);
   const int T = 256;
   const unsigned gs = static_cast<unsigned>((nseg + T - 1) / T), go = (nobj + T - 1) / T;
+  const unsigned gc = static_cast<unsigned>((nchunk + T - 1) / T);
+  auto L = [] { count_launch(); };
   if (nseg) {
-    fnv_pass_a<<<gs, T, 0, st>>>(d_objs, nobj, nseg, a);
-    count_launch();
+    fnv_pass_a<<<gs, T, 0, st>>>(d_objs, nobj, nseg, pa); L();
+    fnv_chunk_nib<<<gc, T, 0, st>>>(d_objs, nobj, nchunk, pa, cpi); L();
   }
-  fnv_scan_a<<<go, T, 0, st>>>(d_objs, nobj, d_states, a, lst, lend);
-  count_launch();
+  fnv_chain_nib<<<go, T, 0, st>>>(d_objs, nobj, d_states, cpi, cst, lo_end, 0); L();
   if (nseg) {
-    fnv_pass_b<<<gs, T, 0, st>>>(d_objs, nobj, nseg, lst, b);
-    count_launch();
+    fnv_expand_nib<<<gc, T, 0, st>>>(d_objs, nobj, nchunk, pa, cst, lst, 0); L();
+    fnv_pass_b<<<gs, T, 0, st>>>(d_objs, nobj, nseg, lst, pb); L();
+    fnv_chunk_nib<<<gc, T, 0, st>>>(d_objs, nobj, nchunk, pb, cpi); L();
   }
-  fnv_scan_b<<<go, T, 0, st>>>(d_objs, nobj, d_states, b, lst, lend);
-  count_launch();
+  fnv_chain_nib<<<go, T, 0, st>>>(d_objs, nobj, d_states, cpi, cst, hi_end, 4); L();
   if (nseg) {
-    fnv_pass_c<<<gs, T, 0, st>>>(d_objs, nobj, nseg, lst, a);
-    count_launch();
+    fnv_expand_nib<<<gc, T, 0, st>>>(d_objs, nobj, nchunk, pb, cst, lst, 1); L();
+    fnv_pass_c<<<gs, T, 0, st>>>(d_objs, nobj, nseg, lst, pa); L();
+    fnv_chunk_affine<<<gc, T, 0, st>>>(d_objs, nobj, nchunk, pa, ca, cc); L();
   }
-  fnv_combine<<<go, T, 0, st>>>(d_objs, nobj, d_states, a, lend);
-  count_launch();
+  fnv_combine<<<go, T, 0, st>>>(d_objs, nobj, d_states, ca, cc, lo_end, hi_end, out_mapped); L();
 }
 
 }  // namespace tsb::dev

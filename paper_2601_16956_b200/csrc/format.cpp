@@ -188,6 +188,16 @@ void file_writer::map_fixed_region() {
   map_ = static_cast<uint8_t*>(m);
 }
 
+#ifndef MADV_POPULATE_WRITE
+#define MADV_POPULATE_WRITE 23
+#endif
+void file_writer::populate(uint64_t off, uint64_t n) {
+  if (!map_ || off >= tre_) return;
+  n = std::min<uint64_t>(n, tre_ - off);
+  const uint64_t a = off & ~4095ull;
+  ::madvise(map_ + a, n + (off - a), MADV_POPULATE_WRITE);  // best effort
+}
+
 void file_writer::write_fixed(uint64_t off, const void* p, size_t n) {
   if (!io_ || n == 0) return;
   if (off < header_reserved || off + n > tre_) fail(TS_ERR_IO, "fixed write outside the tensor region");

@@ -60,6 +60,10 @@ class file_writer {
   // lock), but page faults and copies into a shared mapping proceed in
   // parallel, so many flush threads can fill one file concurrently.
   void map_fixed_region();
+  bool mapped() const { return map_ != nullptr; }
+  // Pre-faults [off, off+n) of the mapping (MADV_POPULATE_WRITE): page
+  // allocation for the file overlaps the device-side capture and D2H.
+  void populate(uint64_t off, uint64_t n);
   void write_fixed(uint64_t off, const void* p, size_t n);
   void finalize_at(uint64_t off, const std::vector<footer_entry>& entries);
   const std::string& path() const { return path_; }

@@ -63,12 +63,17 @@ constexpr uint64_t kFnvSeg = 16384;
 struct fnv_obj {
   const uint8_t* ptr;
   uint64_t len;
-  uint64_t seg0;  // first global segment index (prefix sum of ceil(len / kFnvSeg))
+  uint64_t seg0;    // first global segment index (prefix sum of ceil(len / kFnvSeg))
+  uint64_t chunk0;  // first global chunk index (chunks of 64 segments, per object)
 };
 inline uint64_t align_up_dev(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
-uint64_t fnv_scratch_bytes(uint64_t nseg, uint32_t nobj);
-void launch_fnv(const fnv_obj* d_objs, uint32_t nobj, uint64_t nseg, uint64_t* d_states, void* d_scratch,
-                cudaStream_t st);
+// Fills seg0/chunk0 of a host table; returns the segment count, *nchunk the chunk count.
+uint64_t fnv_prepare(fnv_obj* objs, uint32_t n, uint64_t* nchunk);
+uint64_t fnv_scratch_bytes(uint64_t nseg, uint64_t nchunk, uint32_t nobj);
+// 11 launches on `st`; d_states (in: chain start, out: FNV state) per object;
+// results also stored to `out_mapped` (device view of mapped pinned memory) if set.
+void launch_fnv(const fnv_obj* d_objs, uint32_t nobj, uint64_t nseg, uint64_t nchunk, uint64_t* d_states,
+                void* d_scratch, cudaStream_t st, uint64_t* out_mapped = nullptr);
 
 int sm_count(int device);
 unsigned long long launches();

@@ -345,20 +345,22 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
   if (!dev_objs.empty() && S.err_status == TS_OK) {
     std::vector<dev::fnv_obj> fo(dev_objs.size());
     std::vector<uint64_t> seeds(dev_objs.size(), fnv_seed);
-    uint64_t nseg = 0;
     for (size_t i = 0; i < dev_objs.size(); ++i) {
       const auto& o = objs[dev_objs[i]];
-      fo[i] = {static_cast<const uint8_t*>(o.d->data), o.size, nseg};
-      nseg += (o.size + dev::kFnvSeg - 1) / dev::kFnvSeg;
+      fo[i] = {static_cast<const uint8_t*>(o.d->data), o.size, 0, 0};
     }
     const uint32_t nf = static_cast<uint32_t>(fo.size());
+    uint64_t nchunk = 0;
+    const uint64_t nseg = dev::fnv_prepare(fo.data(), nf, &nchunk);
     const uint64_t tb = align_up(nf * sizeof(dev::fnv_obj), 256), sb = align_up(nf * 8ull, 256);
     uint8_t* fb = nullptr;
-    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&fb), tb + sb + dev::fnv_scratch_bytes(nseg, nf), st), "alloc");
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&fb), tb + sb + dev::fnv_scratch_bytes(nseg, nchunk, nf), st),
+               "alloc");
     cuda_check(cudaMemcpyAsync(fb, fo.data(), nf * sizeof(dev::fnv_obj), cudaMemcpyHostToDevice, st), "upload");
     cuda_check(cudaMemcpyAsync(fb + tb, seeds.data(), nf * 8ull, cudaMemcpyHostToDevice, st), "upload");
-    dev::launch_fnv(reinterpret_cast<dev::fnv_obj*>(fb), nf, nseg, reinterpret_cast<uint64_t*>(fb + tb), fb + tb + sb, st);
-    launches += 6;
+    dev::launch_fnv(reinterpret_cast<dev::fnv_obj*>(fb), nf, nseg, nchunk, reinterpret_cast<uint64_t*>(fb + tb),
+                    fb + tb + sb, st);
+    launches += 11;
     cuda_check(cudaGetLastError(), "checksum kernels");
     cuda_check(cudaMemcpyAsync(dev_ck.data(), fb + tb, nf * 8ull, cudaMemcpyDeviceToHost, st), "download");
     cuda_check(cudaFreeAsync(fb, st), "free");

@@ -33,5 +33,6 @@ for it in (2, 3):
     t = eng.issue_checkpoint(sess, st, it)
     t.wait_persisted()
     s = t.stats()
-    print({k: s[k] for k in ("image_bytes", "pack_ms", "d2h_ms", "t_snapshot_ns", "kernel_launches")})
+    print({k: s[k] for k in ("image_bytes", "pack_ms", "d2h_ms", "t_captured_ns", "t_snapshot_ns", "t_persisted_ns",
+                             "kernel_launches")})
 eng.shutdown()
