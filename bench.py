@@ -391,7 +391,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
             it += 1
             api.mutate_update_step(state, it, stream=comp)  # optimizer update
             ib = 0
-            if mode == "lazy":
+            if mode == "lazy" and k % args.ckpt_interval == 0:
                 sess = api.CheckpointSession("", it, it, None, 1, writes_manifest=False)
                 tt = time.perf_counter()
                 pending = eng.issue_checkpoint(sess, state, it, producer_stream=comp)
@@ -399,13 +399,16 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
             torch.cuda.synchronize()
             if k > 0:
                 times.append(time.perf_counter() - t0)
-                blocked.append(1e3 * (b / 1e9 + ib))
+                if mode == "lazy" and k % args.ckpt_interval == 0:
+                    blocked.append(1e3 * (b / 1e9 + ib))
+                elif b and blocked:
+                    blocked[-1] += 1e3 * b / 1e9  # barrier wait attributed to its checkpoint
         if pending:
             pending.wait_persisted()
-        res[mode] = (statistics.mean(times), statistics.mean(blocked))
+        res[mode] = (statistics.mean(times), statistics.mean(blocked) if blocked else 0.0)
     eng.shutdown()
     off, lazy = res["off"][0], res["lazy"][0]
-    return {"fwd_bwd_ms": round(fb_ms, 1), "steps": args.train_steps,
+    return {"fwd_bwd_ms": round(fb_ms, 1), "steps": args.train_steps, "ckpt_interval": args.ckpt_interval,
             "step_ms_no_ckpt": round(1e3 * off, 2), "step_ms_lazy_ckpt": round(1e3 * lazy, 2),
             "slowdown_pct": round(100 * (lazy - off) / off, 2),
             "blocked_ms_per_ckpt": round(res["lazy"][1], 3)}
@@ -422,6 +425,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--train-steps", type=int, default=3)
     ap.add_argument("--fwd-bwd-ms", type=float, default=1800.0)
+    ap.add_argument("--ckpt-interval", type=int, default=1, help="checkpoint every k training steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pool-gb", type=float, default=0.0, help="pinned pool cap (default: image, at most 64 GiB)")
     ap.add_argument("--ring-gb", type=float, default=8.0, help="HBM staging ring when no full device shadow fits")

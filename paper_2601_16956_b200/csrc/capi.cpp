@@ -555,7 +555,7 @@ ts_status ts_fnv1a64_device(const void* const* ptrs, const uint64_t* sizes, size
     std::vector<dev::fnv_obj> objs(n);
     std::vector<uint64_t> states(n);
     for (size_t i = 0; i < n; ++i) {
-      objs[i] = {static_cast<const uint8_t*>(ptrs[i]), sizes[i], 0, 0};
+      objs[i] = {static_cast<const uint8_t*>(ptrs[i]), sizes[i], 0, 0, i};
       states[i] = init ? init[i] : fnv_seed;
     }
     uint64_t nchunk = 0;

@@ -266,6 +266,7 @@ struct job {
   std::vector<sobj> sobjs;
   std::vector<dev::seg> segs;
   std::vector<cudaEvent_t> chunk_events;  // per-job, destroyed at the end
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pack_events;  // kernel-only pack timing
   uint64_t img = 0;
   bool io = true;
   // device checksums (checksum_on_gpu): device-tier raw objects hashed by the
@@ -276,8 +277,17 @@ struct job {
   std::vector<uint32_t> worder;
   bool gpu_ck = false;
   std::vector<uint32_t> fnv_objs;
-  pinned_pool::region fnv_r;
+  uint64_t* fnv_out = nullptr;  // engine's mapped results buffer
   cudaEvent_t fnv_ev = nullptr;
+
+  ~job() {
+    for (auto e : chunk_events)
+      if (e) cudaEventDestroy(e);
+    for (auto& pe : pack_events) {
+      cudaEventDestroy(pe.first);
+      cudaEventDestroy(pe.second);
+    }
+  }
 
   std::mutex mu;
   size_t wins_landed = 0, wins_enqueued = 0, structs_pending = 0, files_done = 0;
@@ -331,6 +341,7 @@ engine::~engine() {
   if (ring_) cudaFree(ring_);
   if (segbuf_) cudaFree(segbuf_);
   if (fnvbuf_) cudaFree(fnvbuf_);
+  if (ck_host_) cudaFreeHost(ck_host_);
   if (pack_stream_) cudaStreamDestroy(pack_stream_);
   if (copy_stream_) cudaStreamDestroy(copy_stream_);
   for (auto e : ev_free_) cudaEventDestroy(e);
@@ -698,11 +709,13 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     return t.failed;
   };
 
-  // Device staging plan (RING): whole image when it fits (device shadow), else
-  // two slots of whole windows with the packs running ahead of the copies.
+  // Device staging plan (RING): the whole image when it fits (device shadow);
+  // else a ring of `nslots` chunks of whole windows (>= 1 GiB each when the
+  // ring allows), packs running ahead of the copies, so the capture completes
+  // once all but the last ring-full of the image has left the device.
   const uint64_t W = j->wins.empty() ? 0 : j->wins.front().hi - j->wins.front().lo;
   uint64_t chunk = 0;
-  int nslots = 0;
+  size_t nslots = 0, nchunks = 0;
   uint8_t* ring = nullptr;
   if (mode == TS_D2H_RING && j->img > 0) {
     const uint64_t want = align_up(j->img, 256);
@@ -711,12 +724,13 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       chunk = want;
       nslots = 1;
     } else {
-      chunk = std::max<uint64_t>(W, (cap / 2) / W * W);
-      nslots = 2;
+      chunk = std::max<uint64_t>(W, std::min<uint64_t>(1ull << 30, cap / 2) / W * W);
+      nslots = static_cast<size_t>(cap / chunk);
     }
-    ring = ensure_device_ring(nslots == 1 ? want : 2 * chunk);
+    nchunks = (j->img + chunk - 1) / chunk;
+    ring = ensure_device_ring(nslots == 1 ? want : nslots * chunk);
   }
-  const bool shadow = nslots == 1;
+  const bool use_ring = ring != nullptr;
 
   dev::seg* d_segs = nullptr;
   if (j->img > 0 && mode != TS_D2H_DIRECT) {
@@ -725,39 +739,82 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     cuda_check(cudaMemcpyAsync(d_segs, j->segs.data(), j->segs.size() * sizeof(dev::seg),
                                cudaMemcpyHostToDevice, pack_stream_), "upload segment table");
   }
-  // Device checksums: over the device shadow after the pack (off the capture
-  // path), else over the state itself before the capture completes.
+  // Device checksums. RING: per chunk over the ring slot right after its pack
+  // (chained states, off the capture path). DIRECT / ZEROCOPY: over the state
+  // itself before the capture completes. Table: one entry per (chunk, object
+  // piece), grouped by chunk; launch k covers entries [cbeg[k], cbeg[k+1]).
   const uint32_t nf = static_cast<uint32_t>(j->fnv_objs.size());
   uint8_t* fbuf = nullptr;
-  uint64_t fnseg = 0, fnchunk = 0, ftb = 0, fsb = 0;
+  uint64_t ftb = 0, fsb = 0;
+  std::vector<dev::fnv_obj> fo;
+  std::vector<size_t> cbeg;
+  std::vector<std::pair<uint64_t, uint64_t>> cdims;  // (nseg, nchunk) per launch
   if (nf) {
-    std::vector<dev::fnv_obj> fo(nf);
-    std::vector<uint64_t> st(nf, fnv_seed);
-    for (uint32_t i = 0; i < nf; ++i) {
-      const auto& r = j->raws[j->fnv_objs[i]];
-      fo[i] = {shadow ? ring + r.img : r.src, r.size, 0, 0};
+    if (use_ring) {
+      size_t k = 0;  // fnv_objs are in image order
+      for (size_t c = 0; c < nchunks; ++c) {
+        cbeg.push_back(fo.size());
+        const uint64_t clo = c * chunk, chi = std::min(j->img, clo + chunk);
+        while (k < nf && j->raws[j->fnv_objs[k]].img + j->raws[j->fnv_objs[k]].size <= clo) ++k;
+        for (size_t q = k; q < nf && j->raws[j->fnv_objs[q]].img < chi; ++q) {
+          const auto& r = j->raws[j->fnv_objs[q]];
+          const uint64_t a = std::max(clo, r.img), b = std::min(chi, r.img + r.size);
+          fo.push_back({ring + (nslots == 1 ? 0 : (c % nslots) * chunk) + (a - clo), b - a, 0, 0, q});
+        }
+      }
+      cbeg.push_back(fo.size());
+    } else {
+      for (uint32_t q = 0; q < nf; ++q) {
+        const auto& r = j->raws[j->fnv_objs[q]];
+        fo.push_back({r.src, r.size, 0, 0, q});
+      }
+      cbeg = {0, fo.size()};
     }
-    fnseg = dev::fnv_prepare(fo.data(), nf, &fnchunk);
-    ftb = align_up(nf * sizeof(dev::fnv_obj), 256);
+    uint64_t max_scratch = 0;
+    for (size_t k = 0; k + 1 < cbeg.size(); ++k) {
+      uint64_t nch = 0;
+      const uint32_t cnt = static_cast<uint32_t>(cbeg[k + 1] - cbeg[k]);
+      const uint64_t nseg = dev::fnv_prepare(fo.data() + cbeg[k], cnt, &nch);
+      cdims.push_back({nseg, nch});
+      max_scratch = std::max(max_scratch, dev::fnv_scratch_bytes(nseg, nch, cnt));
+    }
+    ftb = align_up(fo.size() * sizeof(dev::fnv_obj), 256);
     fsb = align_up(nf * 8ull, 256);
-    fbuf = ensure_fnv_buffer(ftb + fsb + dev::fnv_scratch_bytes(fnseg, fnchunk, nf));
-    cuda_check(cudaMemcpyAsync(fbuf, fo.data(), nf * sizeof(dev::fnv_obj), cudaMemcpyHostToDevice, pack_stream_),
-               "upload checksum table");
-    cuda_check(cudaMemcpyAsync(fbuf + ftb, st.data(), nf * 8ull, cudaMemcpyHostToDevice, pack_stream_),
+    fbuf = ensure_fnv_buffer(ftb + fsb + max_scratch);
+    std::vector<uint64_t> seeds(nf, fnv_seed);
+    cuda_check(cudaMemcpyAsync(fbuf, fo.data(), fo.size() * sizeof(dev::fnv_obj), cudaMemcpyHostToDevice,
+                               pack_stream_), "upload checksum table");
+    cuda_check(cudaMemcpyAsync(fbuf + ftb, seeds.data(), nf * 8ull, cudaMemcpyHostToDevice, pack_stream_),
                "upload checksum seeds");
-    j->fnv_r = pool_->acquire(nf * 8ull, timeout >= 0 ? now_ns() + timeout : -1);
+    if (ck_host_n_ < nf) {  // the previous job's results were consumed before its snapshot completed
+      if (ck_host_) cudaFreeHost(ck_host_);
+      ck_host_ = nullptr;
+      cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&ck_host_), nf * 8ull, cudaHostAllocMapped | cudaHostAllocPortable),
+                 "cudaHostAlloc(checksums)");
+      ck_host_n_ = nf;
+    }
+    j->fnv_out = ck_host_;
     j->fnv_ev = get_event();
   }
-  auto launch_checksums = [&] {
-    // Results are stored by the last kernel straight into the mapped pool region:
-    // a cudaMemcpy would queue behind the bulk D2H windows on the copy engine.
-    uint64_t* out = nullptr;
-    cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&out), pool_->data(j->fnv_r), 0),
-               "cudaHostGetDevicePointer");
-    dev::launch_fnv(reinterpret_cast<dev::fnv_obj*>(fbuf), nf, fnseg, fnchunk,
-                    reinterpret_cast<uint64_t*>(fbuf + ftb), fbuf + ftb + fsb, pack_stream_, out);
-    t.kernel_launches += 11;
-    cuda_check(cudaGetLastError(), "checksum kernels");
+  // Launch k of the checksum kernels; the last one publishes the results
+  // straight into the mapped pool region (a cudaMemcpy would queue behind the
+  // bulk D2H windows on the copy engine).
+  auto launch_checksums = [&](size_t k) {
+    if (!nf || cbeg[k + 1] == cbeg[k]) {
+      if (nf && k + 2 == cbeg.size()) goto publish;
+      return;
+    }
+    {
+      uint64_t* out = nullptr;
+      cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&out), j->fnv_out, 0), "cudaHostGetDevicePointer");
+      dev::launch_fnv(reinterpret_cast<dev::fnv_obj*>(fbuf) + cbeg[k], static_cast<uint32_t>(cbeg[k + 1] - cbeg[k]),
+                      cdims[k].first, cdims[k].second, reinterpret_cast<uint64_t*>(fbuf + ftb), fbuf + ftb + fsb,
+                      pack_stream_, out);
+      t.kernel_launches += 11;
+      cuda_check(cudaGetLastError(), "checksum kernels");
+    }
+    if (k + 2 != cbeg.size()) return;
+  publish:
     cuda_check(cudaEventRecord(j->fnv_ev, pack_stream_), "event");
     {
       std::lock_guard<std::mutex> g(mu_);
@@ -768,8 +825,8 @@ void engine::run_job(const std::shared_ptr<job>& j) {
   cuda_check(cudaStreamWaitEvent(pack_stream_, t.ev_start, 0), "wait producer");
   cuda_check(cudaStreamWaitEvent(copy_stream_, t.ev_start, 0), "wait producer");
   cuda_check(cudaEventRecord(t.ev_pack0, mode == TS_D2H_DIRECT ? copy_stream_ : pack_stream_), "event");
-  if (nf && !shadow) {
-    launch_checksums();
+  if (nf && !use_ring) {
+    launch_checksums(0);
     // DIRECT captures on the copy stream: it must also cover the checksum reads.
     cuda_check(cudaStreamWaitEvent(copy_stream_, j->fnv_ev, 0), "wait checksums");
   }
@@ -780,15 +837,21 @@ void engine::run_job(const std::shared_ptr<job>& j) {
   const uint32_t nsegs = static_cast<uint32_t>(j->segs.size());
 
   if (mode == TS_D2H_RING) {
-    const size_t nchunks = (j->img + chunk - 1) / chunk;
+    const bool shadow = nslots == 1;
     j->chunk_events.assign(nchunks, nullptr);
     size_t w = 0;
     cuda_check(cudaEventRecord(t.ev_d2h_first, copy_stream_), "event");
     for (size_t c = 0; c < nchunks && !failed(); ++c) {
       const uint64_t clo = c * chunk, chi = std::min(j->img, clo + chunk);
-      uint8_t* slot = ring + (nslots == 1 ? 0 : (c % 2) * chunk);
-      if (c >= 2) cuda_check(cudaStreamWaitEvent(pack_stream_, j->chunk_events[c - 2], 0), "slot wait");
+      uint8_t* slot = ring + (shadow ? 0 : (c % nslots) * chunk);
+      if (c >= nslots) cuda_check(cudaStreamWaitEvent(pack_stream_, j->chunk_events[c - nslots], 0), "slot wait");
+      cudaEvent_t pa, pb;
+      cuda_check(cudaEventCreate(&pa), "event");
+      cuda_check(cudaEventCreate(&pb), "event");
+      cuda_check(cudaEventRecord(pa, pack_stream_), "event");
       dev::launch_pack(d_segs, nsegs, clo, chi, slot, ctas, threads, pack_stream_);
+      cuda_check(cudaEventRecord(pb, pack_stream_), "event");
+      j->pack_events.push_back({pa, pb});
       t.kernel_launches += 1;
       cuda_check(cudaGetLastError(), "pack kernel launch");
       cudaEvent_t packed;
@@ -796,16 +859,17 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       cuda_check(cudaEventRecord(packed, pack_stream_), "event");
       if (c + 1 == nchunks) mark_capture(pack_stream_);
       cuda_check(cudaStreamWaitEvent(copy_stream_, packed, 0), "wait pack");
-      if (nf && shadow) launch_checksums();  // reads the shadow, overlaps the D2H
       cudaEventDestroy(packed);  // destruction is deferred until the event completes
+      if (nf) launch_checksums(c);  // reads the slot, overlaps the D2H; next pack of the slot queues behind
       for (size_t q = w; q < j->wins.size() && j->wins[q].lo < chi; ++q, ++w) {
-        auto& win = j->wins[shadow ? j->worder[q] : q];
+        const size_t wi = shadow ? j->worder[q] : q;
+        auto& win = j->wins[wi];
         acquire(win);
         cuda_check(cudaMemcpyAsync(pool_->data(win.r), slot + (win.lo - clo), win.hi - win.lo,
                                    cudaMemcpyDeviceToHost, copy_stream_), "D2H window");
         t.copies += 1;
         cuda_check(cudaEventRecord(win.ev, copy_stream_), "event");
-        push_window(shadow ? j->worder[q] : q);
+        push_window(wi);
         if (failed()) break;
       }
       cudaEvent_t done;
@@ -881,7 +945,6 @@ void engine::completer_loop() {
       j->fnv_ev = nullptr;
       if (e != cudaSuccess) {
         j->t->fail(TS_ERR_CUDA, std::string("checksum kernels failed: ") + cudaGetErrorString(e));
-        pool_->release(j->fnv_r);
         continue;
       }
       fnv_landed(j);
@@ -949,7 +1012,7 @@ void engine::window_landed(const std::shared_ptr<job>& j, size_t wi) {
 // Device checksums of every device-tier raw object landed (transfer.cpp:71-83's
 // per-object FNV, computed by the FNV kernels instead of the staging thread).
 void engine::fnv_landed(const std::shared_ptr<job>& j) {
-  const auto* res = reinterpret_cast<const uint64_t*>(pool_->data(j->fnv_r));
+  const uint64_t* res = j->fnv_out;
   {
     std::lock_guard<std::mutex> g(j->t->mu);
     for (size_t i = 0; i < j->fnv_objs.size(); ++i) j->t->checksums[j->raws[j->fnv_objs[i]].oid] = res[i];
@@ -961,7 +1024,6 @@ void engine::fnv_landed(const std::shared_ptr<job>& j) {
       j->files[j->raws[k].f].raw_pending -= 1;
     }
   }
-  pool_->release(j->fnv_r);
   TRACE("checksums landed rank=%d objects=%zu", j->rank_id, j->fnv_objs.size());
   for (size_t f = 0; f < j->files.size(); ++f) file_progress(j, f);
 }
@@ -1105,7 +1167,14 @@ void engine::check_snapshot(const std::shared_ptr<job>& j) {
         j->t->snapshot = true;
         j->t->t_snapshot = now_ns() - j->t->t_issue;
         cudaEventElapsedTime(&j->t->d2h_ms, j->t->ev_d2h_first, j->t->ev_d2h_last);
-        cudaEventElapsedTime(&j->t->pack_ms, j->t->ev_pack0, j->t->ev_capture);
+        if (!j->pack_events.empty()) {  // RING: sum of the pack kernels alone
+          float sum = 0, ms = 0;
+          for (auto& pe : j->pack_events)
+            if (cudaEventElapsedTime(&ms, pe.first, pe.second) == cudaSuccess) sum += ms;
+          j->t->pack_ms = sum;
+        } else {
+          cudaEventElapsedTime(&j->t->pack_ms, j->t->ev_pack0, j->t->ev_capture);
+        }
         if (j->t->t_captured < 0) j->t->t_captured = j->t->t_snapshot;
       }
     }
@@ -1162,9 +1231,6 @@ void engine::file_progress(const std::shared_ptr<job>& j, size_t fi) {
     j->t->persisted = true;
     j->t->t_persisted = now_ns() - j->t->t_issue;
   }
-  for (auto e : j->chunk_events)
-    if (e) cudaEventDestroy(e);
-  j->chunk_events.clear();
   try {
     j->sess->rank_persisted(j->rank_id);
   } catch (const error& e) {

@@ -152,6 +152,8 @@ class engine {
   uint64_t segbuf_bytes_ = 0;
   uint8_t* fnvbuf_ = nullptr;
   uint64_t fnvbuf_bytes_ = 0;
+  uint64_t* ck_host_ = nullptr;  // mapped pinned checksum results (not from the staging pool:
+  uint64_t ck_host_n_ = 0;       // holding pool space across the D2H could starve the windows)
 
   std::mutex ev_mu_;
   std::vector<cudaEvent_t> ev_free_;

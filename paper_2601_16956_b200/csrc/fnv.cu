@@ -197,7 +197,7 @@ __global__ void fnv_chain_nib(const fnv_obj* __restrict__ o, uint32_t n,
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint64_t c0 = o[i].chunk0, c1 = c0 + (obj_nseg(o[i]) + kChunk - 1) / kChunk;
-  uint32_t x = static_cast<uint32_t>(states[i] >> shift) & 15u;
+  uint32_t x = static_cast<uint32_t>(states[o[i].sidx] >> shift) & 15u;
   for (uint64_t c = c0; c < c1; ++c) {
     cstart[c] = static_cast<uint8_t>(x);
     x = nib(cpi[c], x);
@@ -259,15 +259,15 @@ __global__ void fnv_combine(const fnv_obj* __restrict__ o, uint32_t n,
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (o[i].len == 0) {
-    if (out) out[i] = states[i];
+    if (out) out[o[i].sidx] = states[o[i].sidx];
     return;
   }
   const uint64_t c0 = o[i].chunk0, c1 = c0 + (obj_nseg(o[i]) + kChunk - 1) / kChunk;
-  uint64_t H = states[i] >> 8;
+  uint64_t H = states[o[i].sidx] >> 8;
   for (uint64_t c = c0; c < c1; ++c) H = (ca[c] * H + cc[c]) & kM56;
   const uint64_t h = (H << 8) | (static_cast<uint64_t>(hi_end[i]) << 4) | lo_end[i];
-  states[i] = h;
-  if (out) out[i] = h;  // mapped pinned memory: no copy-engine round trip behind bulk D2H
+  states[o[i].sidx] = h;
+  if (out) out[o[i].sidx] = h;  // mapped pinned memory: no copy-engine round trip behind bulk D2H
 }
 
 }  // namespace

@@ -65,6 +65,8 @@ struct fnv_obj {
   uint64_t len;
   uint64_t seg0;    // first global segment index (prefix sum of ceil(len / kFnvSeg))
   uint64_t chunk0;  // first global chunk index (chunks of 64 segments, per object)
+  uint64_t sidx;    // index of this range's chain state in d_states / out (pieces of one
+                    // object in later launches continue from the same state)
 };
 inline uint64_t align_up_dev(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 // Fills seg0/chunk0 of a host table; returns the segment count, *nchunk the chunk count.

@@ -347,7 +347,7 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
     std::vector<uint64_t> seeds(dev_objs.size(), fnv_seed);
     for (size_t i = 0; i < dev_objs.size(); ++i) {
       const auto& o = objs[dev_objs[i]];
-      fo[i] = {static_cast<const uint8_t*>(o.d->data), o.size, 0, 0};
+      fo[i] = {static_cast<const uint8_t*>(o.d->data), o.size, 0, 0, i};
     }
     const uint32_t nf = static_cast<uint32_t>(fo.size());
     uint64_t nchunk = 0;
