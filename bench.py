@@ -208,7 +208,8 @@ def ours(args):
     pool = (min(img_est + (64 << 20), pool_cap) + (2 << 20) - 1) // (2 << 20) * (2 << 20)
     cfg = api.EngineConfig(d2h_mode=args.mode, staging_capacity_bytes=pool, raw_chunk_bytes=64 << 20,
                            device_staging_bytes=img_est + (1 << 20) if shadow else int(args.ring_gb * (1 << 30)),
-                           flush_workers=min(16, os.cpu_count() or 8), write_files=False)
+                           flush_workers=min(16, os.cpu_count() or 8), write_files=False,
+                           checksum_on_gpu=not args.host_checksum)
     eng = api.CheckpointEngine(cfg, spec.rank_id, local)
     full = getattr(rec, "full_layout", None)
     echo = S.Recipe(layout=full).manifest_echo() if full else rec.manifest_echo()
@@ -347,7 +348,8 @@ def ours(args):
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": f"{args.config}: {rec.name} rank-r shard, {len(spec.objects)} objects, "
                                    f"{bytes_step / 1e9:.3f} GB/rank", "d2h_mode": args.mode,
-                       "device_shadow": bool(shadow), "pinned_pool_gb": round(pool / 2**30, 2), "l2": "inputs > L2 (126 MB)",
+                       "device_shadow": bool(shadow), "pinned_pool_gb": round(pool / 2**30, 2),
+                       "checksums": "host" if args.host_checksum else "gpu", "l2": "inputs > L2 (126 MB)",
                        "step": "update(pattern kernel) + issue + snapshot + checksums (no files)"},
             "per_gpu_gbps": round(value / ws, 3),
             "snapshot_ms_mean": round(statistics.mean(snap_ms), 2),
@@ -378,15 +380,17 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
     run, fb_ms = gemm_load(args.fwd_bwd_ms, dev)
     eng = api.CheckpointEngine(cfg, spec.rank_id, local)
     comp = torch.cuda.current_stream()
-    res = {}
-    for mode in ("off", "lazy"):
+    res = {"off": ([], []), "lazy": ([], [])}
+    it = it0
+    # off/lazy blocks alternate (twice) so clock / power-cap drift hits both arms
+    for mode in ("off", "lazy", "off", "lazy"):
         pending = None
-        it = it0 + (100 if mode == "lazy" else 0)
-        times, blocked = [], []
+        times, blocked = res[mode]
         for k in range(args.train_steps + 1):
-            torch.cuda.synchronize()
+            comp.synchronize()  # like a per-step loss.item(): the compute stream only, never the device
             t0 = time.perf_counter()
             run()                                    # forward + backward
+            comp.synchronize()  # fwd/bwd done (the simulator's synchronous phases, simulator.cpp:129-130)
             b = eng.pre_update_barrier(pending, stream=comp, host_block=1) if pending else 0
             it += 1
             api.mutate_update_step(state, it, stream=comp)  # optimizer update
@@ -396,7 +400,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
                 tt = time.perf_counter()
                 pending = eng.issue_checkpoint(sess, state, it, producer_stream=comp)
                 ib = time.perf_counter() - tt
-            torch.cuda.synchronize()
+            comp.synchronize()
             if k > 0:
                 times.append(time.perf_counter() - t0)
                 if mode == "lazy" and k % args.ckpt_interval == 0:
@@ -405,10 +409,10 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
                     blocked[-1] += 1e3 * b / 1e9  # barrier wait attributed to its checkpoint
         if pending:
             pending.wait_persisted()
-        res[mode] = (statistics.mean(times), statistics.mean(blocked) if blocked else 0.0)
+    res = {m: (statistics.mean(t), statistics.mean(b) if b else 0.0) for m, (t, b) in res.items()}
     eng.shutdown()
     off, lazy = res["off"][0], res["lazy"][0]
-    return {"fwd_bwd_ms": round(fb_ms, 1), "steps": args.train_steps, "ckpt_interval": args.ckpt_interval,
+    return {"fwd_bwd_ms": round(fb_ms, 1), "steps": 2 * args.train_steps, "ckpt_interval": args.ckpt_interval,
             "step_ms_no_ckpt": round(1e3 * off, 2), "step_ms_lazy_ckpt": round(1e3 * lazy, 2),
             "slowdown_pct": round(100 * (lazy - off) / off, 2),
             "blocked_ms_per_ckpt": round(res["lazy"][1], 3)}
@@ -426,6 +430,7 @@ def main():
     ap.add_argument("--train-steps", type=int, default=3)
     ap.add_argument("--fwd-bwd-ms", type=float, default=1800.0)
     ap.add_argument("--ckpt-interval", type=int, default=1, help="checkpoint every k training steps")
+    ap.add_argument("--host-checksum", action="store_true", help="FNV on host threads instead of the GPU kernels")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pool-gb", type=float, default=0.0, help="pinned pool cap (default: image, at most 64 GiB)")
     ap.add_argument("--ring-gb", type=float, default=8.0, help="HBM staging ring when no full device shadow fits")

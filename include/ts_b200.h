@@ -163,7 +163,10 @@ typedef struct ts_engine_config {
   uint64_t hybrid_direct_min_bytes; /* HYBRID threshold */
   int32_t pack_ctas;                /* 0 = auto (one per SM) */
   int32_t pack_threads;             /* threads per pack CTA, default 512 */
-  int32_t low_priority_stream;      /* snapshot streams at the lowest priority, default 1 */
+  int32_t pack_priority;            /* capture (pack + checksum) stream priority: 1 highest (default:
+                                       the capture is latency-critical and must not starve behind
+                                       back-to-back compute kernels), 0 default, -1 lowest; the D2H
+                                       copy stream always runs at the lowest priority */
   int32_t write_files;              /* 0 = snapshot-only run (no file I/O, bench only) */
   int32_t checksum_on_gpu;          /* 1 (default): exact segment-parallel FNV-1a kernels on the
                                        device copy; 0: host threads over the pinned pool */

@@ -99,7 +99,7 @@ class EngineConfigC(C.Structure):
                 ("alignment", C.c_uint64), ("cache_acquire_timeout_ns", C.c_int64),
                 ("overwrite", C.c_int32), ("d2h_mode", C.c_int32), ("device_staging_bytes", C.c_uint64),
                 ("hybrid_direct_min_bytes", C.c_uint64), ("pack_ctas", C.c_int32),
-                ("pack_threads", C.c_int32), ("low_priority_stream", C.c_int32), ("write_files", C.c_int32),
+                ("pack_threads", C.c_int32), ("pack_priority", C.c_int32), ("write_files", C.c_int32),
                 ("checksum_on_gpu", C.c_int32), ("flush_mmap", C.c_int32)]
 
 

@@ -252,7 +252,7 @@ class EngineConfig:
     hybrid_direct_min_bytes: int = 64 << 20
     pack_ctas: int = 0
     pack_threads: int = 512
-    low_priority_stream: bool = True
+    pack_priority: int = 1  # capture stream: 1 high (default), 0 normal, -1 low
     write_files: bool = True
     checksum_on_gpu: bool = True
     flush_mmap: bool = True
@@ -274,7 +274,7 @@ class EngineConfig:
         c.hybrid_direct_min_bytes = self.hybrid_direct_min_bytes
         c.pack_ctas = self.pack_ctas
         c.pack_threads = self.pack_threads
-        c.low_priority_stream = int(self.low_priority_stream)
+        c.pack_priority = int(self.pack_priority)
         c.write_files = int(self.write_files)
         c.checksum_on_gpu = int(self.checksum_on_gpu)
         c.flush_mmap = int(self.flush_mmap)

@@ -191,7 +191,7 @@ void ts_engine_config_default(ts_engine_config* c) {
   c->hybrid_direct_min_bytes = 64ull << 20;
   c->pack_ctas = 0;
   c->pack_threads = 512;
-  c->low_priority_stream = 1;
+  c->pack_priority = 1;
   c->write_files = 1;
   c->checksum_on_gpu = 1;
   c->flush_mmap = 1;

@@ -207,7 +207,7 @@ struct job {
     bool device = true;
     // checksum actor state (pieces arrive in object order)
     uint64_t fnv = fnv_seed, hashed = 0;
-    bool busy = false;
+    bool busy = false, queued = false;
     struct piece {
       const uint8_t* p;
       uint64_t len;
@@ -264,6 +264,7 @@ struct job {
   std::vector<fseg> fs;
   std::vector<hpiece> hp;
   std::vector<sobj> sobjs;
+  std::deque<uint32_t> ready;  // host-hashed objects with landed, unhashed pieces
   std::vector<dev::seg> segs;
   std::vector<cudaEvent_t> chunk_events;  // per-job, destroyed at the end
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pack_events;  // kernel-only pack timing
@@ -327,9 +328,12 @@ engine::engine(const ts_engine_config& cfg, int rank_id, int device)
   pool_ = std::make_unique<pinned_pool>(cfg_.staging_capacity_bytes);
   int lo_prio = 0, hi_prio = 0;
   cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
-  const int prio = cfg_.low_priority_stream ? lo_prio : hi_prio;
-  cuda_check(cudaStreamCreateWithPriority(&pack_stream_, cudaStreamNonBlocking, prio), "stream");
-  cuda_check(cudaStreamCreateWithPriority(&copy_stream_, cudaStreamNonBlocking, prio), "stream");
+  // Capture kernels preempt compute at CTA granularity (high priority): at low
+  // priority they starve behind back-to-back training kernels and the capture,
+  // hence the pre-update barrier, slips. Copies use the copy engines only.
+  const int pack_prio = cfg_.pack_priority > 0 ? hi_prio : cfg_.pack_priority < 0 ? lo_prio : 0;
+  cuda_check(cudaStreamCreateWithPriority(&pack_stream_, cudaStreamNonBlocking, pack_prio), "stream");
+  cuda_check(cudaStreamCreateWithPriority(&copy_stream_, cudaStreamNonBlocking, lo_prio), "stream");
   workers_ = std::make_unique<thread_pool>(cfg_.flush_workers);
   copier_ = std::thread([this] { copier_loop(); });
   completer_ = std::thread([this] { completer_loop(); });
@@ -978,7 +982,7 @@ void engine::window_landed(const std::shared_ptr<job>& j, size_t wi) {
   uint8_t* base = pool_->data(w.r);
   for (uint32_t k = w.hp_begin; k < w.hp_end; ++k)
     std::memcpy(base + j->hp[k].win_off, j->hp[k].src, j->hp[k].len);  // host-tier bytes
-  std::vector<uint32_t> sched;
+  size_t newly_ready = 0;
   bool release_now = false;
   {
     std::lock_guard<std::mutex> g(j->mu);
@@ -988,9 +992,10 @@ void engine::window_landed(const std::shared_ptr<job>& j, size_t wi) {
       if (j->gpu_ck && r.device) continue;  // checksummed on the device
       w.refs += 1;
       r.q.push_back({base + j->wp[k].win_off, j->wp[k].len, static_cast<uint32_t>(wi)});
-      if (!r.busy) {
-        r.busy = true;
-        sched.push_back(j->wp[k].obj);
+      if (!r.busy && !r.queued) {
+        r.queued = true;
+        j->ready.push_back(j->wp[k].obj);
+        ++newly_ready;
       }
     }
     j->wins_landed += 1;
@@ -1004,7 +1009,8 @@ void engine::window_landed(const std::shared_ptr<job>& j, size_t wi) {
   }
   if (last)
     for (size_t f = 0; f < j->files.size(); ++f) file_progress(j, f);
-  for (uint32_t o : sched) workers_->submit(guarded(j, [this, j, o] { hash_task(j, o); }));
+  for (size_t k = 0; k < (newly_ready + 3) / 4; ++k)
+    workers_->submit(guarded(j, [this, j] { hash_task(j, 0); }));
   if (j->io && w.fs_end > w.fs_begin) workers_->submit(guarded(j, [this, j, wi] { flush_window(j, wi); }));
   check_snapshot(j);
 }
@@ -1037,34 +1043,126 @@ void engine::window_release_ref(const std::shared_ptr<job>& j, size_t wi) {
   if (rel) pool_->release(j->wins[wi].r);
 }
 
-// Object checksum actor: consumes landed pieces of one raw object in order
-// (transfer.cpp:71-83 without the global monitor; objects hash in parallel).
-void engine::hash_task(const std::shared_ptr<job>& j, size_t oi) {
-  auto& r = j->raws[oi];
-  for (;;) {
-    job::rawo::piece p;
-    {
-      std::lock_guard<std::mutex> g(j->mu);
-      if (r.q.empty()) {
-        r.busy = false;
-        return;
+namespace {
+// Advances k (1..4) independent FNV-1a chains by n bytes each, in lock-step:
+// one chain is a 64-bit multiply latency chain (~4 cycles/byte); four give the
+// core instruction-level parallelism.
+void fnv_lockstep(const uint8_t* const* p, uint64_t* h, int k, uint64_t n) {
+  switch (k) {
+    case 4: {
+      uint64_t a = h[0], b = h[1], c = h[2], d = h[3];
+      const uint8_t *pa = p[0], *pb = p[1], *pc = p[2], *pd = p[3];
+      for (uint64_t i = 0; i < n; ++i) {
+        a = (a ^ pa[i]) * fnv_prime;
+        b = (b ^ pb[i]) * fnv_prime;
+        c = (c ^ pc[i]) * fnv_prime;
+        d = (d ^ pd[i]) * fnv_prime;
       }
-      p = r.q.front();
-      r.q.pop_front();
+      h[0] = a, h[1] = b, h[2] = c, h[3] = d;
+      return;
     }
-    r.fnv = fnv1a64(p.p, p.len, r.fnv);
-    const bool done = r.hashed + p.len == r.size;
-    if (done) {  // publish the checksum before the file can see raw_pending == 0
-      std::lock_guard<std::mutex> g(j->t->mu);
-      j->t->checksums[r.oid] = r.fnv;
+    case 3: {
+      uint64_t a = h[0], b = h[1], c = h[2];
+      const uint8_t *pa = p[0], *pb = p[1], *pc = p[2];
+      for (uint64_t i = 0; i < n; ++i) {
+        a = (a ^ pa[i]) * fnv_prime;
+        b = (b ^ pb[i]) * fnv_prime;
+        c = (c ^ pc[i]) * fnv_prime;
+      }
+      h[0] = a, h[1] = b, h[2] = c;
+      return;
     }
+    case 2: {
+      uint64_t a = h[0], b = h[1];
+      const uint8_t *pa = p[0], *pb = p[1];
+      for (uint64_t i = 0; i < n; ++i) {
+        a = (a ^ pa[i]) * fnv_prime;
+        b = (b ^ pb[i]) * fnv_prime;
+      }
+      h[0] = a, h[1] = b;
+      return;
+    }
+    default:
+      h[0] = fnv1a64(p[0], n, h[0]);
+  }
+}
+}  // namespace
+
+// Host checksum worker (checksum_on_gpu = 0, and host-tier objects): takes up
+// to four objects with landed pieces and hashes them interleaved, each in
+// object order (transfer.cpp:71-83 without the global monitor).
+void engine::hash_task(const std::shared_ptr<job>& j, size_t) {
+  for (;;) {
+    uint32_t ids[4];
+    std::vector<job::rawo::piece> pcs[4];
+    int m = 0;
     {
       std::lock_guard<std::mutex> g(j->mu);
-      r.hashed += p.len;
-      if (done) j->files[r.f].raw_pending -= 1;
+      while (m < 4 && !j->ready.empty()) {
+        const uint32_t o = j->ready.front();
+        j->ready.pop_front();
+        auto& r = j->raws[o];
+        r.queued = false;
+        if (r.busy || r.q.empty()) continue;
+        r.busy = true;
+        pcs[m].assign(r.q.begin(), r.q.end());
+        r.q.clear();
+        ids[m++] = o;
+      }
     }
-    window_release_ref(j, p.w);
-    if (done) file_progress(j, r.f);
+    if (m == 0) return;
+    uint64_t h[4];
+    size_t pi[4] = {0, 0, 0, 0};
+    uint64_t off[4] = {0, 0, 0, 0};
+    for (int k = 0; k < m; ++k) h[k] = j->raws[ids[k]].fnv;
+    for (;;) {
+      int act[4], na = 0;
+      for (int k = 0; k < m; ++k)
+        if (pi[k] < pcs[k].size()) act[na++] = k;
+      if (na == 0) break;
+      uint64_t n = UINT64_MAX;
+      const uint8_t* ptr[4];
+      uint64_t hh[4];
+      for (int q = 0; q < na; ++q) {
+        const int k = act[q];
+        n = std::min<uint64_t>(n, pcs[k][pi[k]].len - off[k]);
+        ptr[q] = pcs[k][pi[k]].p + off[k];
+        hh[q] = h[k];
+      }
+      fnv_lockstep(ptr, hh, na, n);
+      for (int q = 0; q < na; ++q) {
+        const int k = act[q];
+        h[k] = hh[q];
+        off[k] += n;
+        if (off[k] == pcs[k][pi[k]].len) {
+          off[k] = 0;
+          ++pi[k];
+        }
+      }
+    }
+    for (int k = 0; k < m; ++k) {
+      auto& r = j->raws[ids[k]];
+      uint64_t len = 0;
+      for (const auto& pc : pcs[k]) len += pc.len;
+      const bool done = r.hashed + len == r.size;
+      r.fnv = h[k];
+      if (done) {  // publish the checksum before the file can see raw_pending == 0
+        std::lock_guard<std::mutex> g(j->t->mu);
+        j->t->checksums[r.oid] = r.fnv;
+      }
+      {
+        std::lock_guard<std::mutex> g(j->mu);
+        r.hashed += len;
+        r.busy = false;
+        if (done) j->files[r.f].raw_pending -= 1;
+        if (!r.q.empty() && !r.queued) {
+          r.queued = true;
+          j->ready.push_back(ids[k]);
+        }
+      }
+      for (const auto& pc : pcs[k]) window_release_ref(j, pc.w);
+      if (done) file_progress(j, r.f);
+    }
   }
 }
 
