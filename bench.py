@@ -299,6 +299,8 @@ def ours(args):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e2e_ms = float(tt.item())
         e2e = {"value": round(box_bytes * args.e2e_steps / (e2e_ms / 1e3) / 1e9, 3), "unit": "GB/s",
+               "persist_ms_last": round(st["t_persisted_ns"] / 1e6, 1),
+               "snapshot_ms_last": round(st["t_snapshot_ns"] / 1e6, 1),
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(image),
                "what": "issue -> files + footers + MANIFEST.tlv durable on /dev/shm, via the C-ABI"}
         # restore of the last checkpoint (H2D + scatter-unpack + FNV verify)

@@ -435,6 +435,20 @@ void require_device() {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     fail(TS_ERR_CUDA, "no CUDA device: the B200 kernels have no CPU fallback");
+  // The small per-call tables below come from the stream-ordered allocator: keep
+  // its memory cached instead of unmapping it at every synchronization.
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = 256ull << 20;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done.push_back(dev);
 }
 }  // namespace
 

@@ -1315,7 +1315,6 @@ void engine::file_progress(const std::shared_ptr<job>& j, size_t fi) {
     j->t->fail(e.status, std::string("finalize failed: ") + e.what(), e.object_id);
     return;
   }
-  f.w.reset();  // close the descriptor
   bool all = false;
   {
     std::lock_guard<std::mutex> g(j->mu);
@@ -1323,7 +1322,10 @@ void engine::file_progress(const std::shared_ptr<job>& j, size_t fi) {
     all = ++j->files_done == j->files.size() && !j->persisted;
     if (all) j->persisted = true;
   }
-  if (!all) return;
+  if (!all) {
+    f.w.reset();  // unmap + close
+    return;
+  }
   {
     std::lock_guard<std::mutex> g(j->t->mu);
     j->t->persisted = true;
@@ -1335,6 +1337,7 @@ void engine::file_progress(const std::shared_ptr<job>& j, size_t fi) {
     j->t->fail(e.status, std::string("manifest failed: ") + e.what());
   }
   j->t->cv.notify_all();
+  f.w.reset();  // unmap + close after the waiters are released
 }
 
 // ---------------------------------------------------------------------------

@@ -177,6 +177,11 @@ file_writer::~file_writer() {
   if (fd_ >= 0) ::close(fd_);
 }
 
+void file_writer::release_mapping() {
+  if (map_) ::munmap(map_, tre_);
+  map_ = nullptr;
+}
+
 void file_writer::map_fixed_region() {
   if (!io_ || map_ || tre_ <= header_reserved) return;
   // A fault on a full filesystem raises SIGBUS instead of returning ENOSPC:
@@ -213,10 +218,6 @@ void file_writer::write_at(uint64_t off, const void* p, size_t n) {
 void file_writer::finalize_at(uint64_t off, const std::vector<footer_entry>& entries) {
   validate_entries(entries, tre_);
   if (!io_) return;
-  if (map_) {
-    ::munmap(map_, tre_);
-    map_ = nullptr;
-  }
   const auto blob = footer_blob(entries);
   pwrite_all(fd_, blob.data(), blob.size(), off, path_);
 }

@@ -66,6 +66,9 @@ class file_writer {
   void populate(uint64_t off, uint64_t n);
   void write_fixed(uint64_t off, const void* p, size_t n);
   void finalize_at(uint64_t off, const std::vector<footer_entry>& entries);
+  // Drops the fixed-region mapping (page-table teardown of a multi-GB mapping
+  // is not free: done after the file is reported persisted).
+  void release_mapping();
   const std::string& path() const { return path_; }
 
  private:

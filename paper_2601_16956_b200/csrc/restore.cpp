@@ -5,6 +5,8 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <unordered_map>
 #include <unordered_set>
 
@@ -14,6 +16,11 @@
 namespace tsb {
 
 namespace {
+
+const bool g_rtrace = std::getenv("TS_TRACE") != nullptr;
+void rtrace(const char* what, int64_t t0) {
+  if (g_rtrace) std::fprintf(stderr, "[ts restore] %-28s %9.3f ms\n", what, (now_ns() - t0) / 1e6);
+}
 
 struct fd_holder {
   int fd = -1;
@@ -26,6 +33,23 @@ struct fd_holder {
 std::mutex g_stage_mu;
 uint8_t* g_pinned = nullptr;
 uint64_t g_pinned_bytes = 0;
+
+// Device window ring, per device, grown on demand and kept (stream-ordered
+// frees of a multi-GB buffer return it to the OS at the next sync: slow).
+std::unordered_map<int, std::pair<uint8_t*, uint64_t>> g_dev_stage, g_dev_scratch;
+uint8_t* device_cached(std::unordered_map<int, std::pair<uint8_t*, uint64_t>>& m, int device, uint64_t bytes) {
+  auto& e = m[device];
+  if (e.second < bytes) {
+    if (e.first) cudaFree(e.first);
+    e.first = nullptr;
+    e.second = 0;
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&e.first), bytes), "cudaMalloc(restore staging)");
+    e.second = bytes;
+  }
+  return e.first;
+}
+uint8_t* device_stage(int device, uint64_t bytes) { return device_cached(g_dev_stage, device, bytes); }
+uint8_t* device_scratch(int device, uint64_t bytes) { return device_cached(g_dev_scratch, device, bytes); }
 
 uint8_t* pinned_stage(uint64_t bytes) {
   if (g_pinned_bytes < bytes) {
@@ -107,6 +131,7 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
                                   cudaStream_t st, ts_restore_stats* stats) {
   const int64_t t_begin = now_ns();
   load_rank(index);
+  rtrace("load_rank", t_begin);
   auto& rc = ranks[static_cast<size_t>(index)];
   const auto& mr = m.ranks[static_cast<size_t>(index)];
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
@@ -171,19 +196,24 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
       usegs.push_back({p.pos, p.len, static_cast<uint8_t*>(const_cast<void*>(o.d->data)) + p.obj_off});
   }
 
-  const uint64_t W = 64ull << 20;
-  const int K = 4;
+  // Pipeline: K pinned windows of W bytes. Reads of a window are cut in 16 MiB
+  // preads spread over the pool; the task finishing a window's last read
+  // enqueues its H2D + scatter-unpack (windows are independent, any order) and
+  // a stream callback frees the slot. Reads run up to K windows ahead.
+  const uint64_t W = 256ull << 20;
+  const int K = 8;
   uint8_t* hring;
   {
     std::lock_guard<std::mutex> g(g_stage_mu);
     hring = pinned_stage(W * K);
   }
+  rtrace("pinned stage", t_begin);
   std::lock_guard<std::mutex> stage_guard(g_stage_mu);  // one restore at a time uses the ring
   uint8_t* dring = nullptr;
   dev::useg* d_usegs = nullptr;
-  cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&dring), W * K, st), "cudaMallocAsync(restore ring)");
+  dring = device_stage(device, W * K);
   if (!usegs.empty()) {
-    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d_usegs), usegs.size() * sizeof(dev::useg), st), "alloc");
+    d_usegs = reinterpret_cast<dev::useg*>(device_scratch(device, usegs.size() * sizeof(dev::useg)));
     cuda_check(cudaMemcpyAsync(d_usegs, usegs.data(), usegs.size() * sizeof(dev::useg),
                                cudaMemcpyHostToDevice, st), "upload unpack table");
   }
@@ -200,13 +230,21 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
   struct shared_state {
     std::mutex mu;
     std::condition_variable cv;
-    int slot_refs[4] = {0, 0, 0, 0};
+    int slot_busy[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     std::string err;
     ts_status err_status = TS_OK;
     int64_t err_oid = -1;
   } S;
   const int nthreads = static_cast<int>(std::min<unsigned>(16, std::max(2u, std::thread::hardware_concurrency())));
-  thread_pool pool(nthreads);
+  struct host_cb_arg {
+    shared_state* s;
+    int slot;
+  };
+  std::vector<host_cb_arg> cb_args(K);
+  for (int k = 0; k < K; ++k) cb_args[k] = {&S, k};
+  std::mutex cuda_mu;  // keeps each window's H2D + unpack + callback contiguous on the stream
+  std::atomic<uint32_t> launches_a{0};
+  const int ctas = dev::sm_count(device) * 2;
   auto set_err = [&](const error& e) {
     std::lock_guard<std::mutex> g(S.mu);
     if (S.err_status == TS_OK) {
@@ -215,124 +253,111 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
       S.err_oid = e.object_id;
     }
   };
-  auto release = [&](int slot) {
-    std::lock_guard<std::mutex> g(S.mu);
-    if (--S.slot_refs[slot] == 0) S.cv.notify_all();
-  };
-  std::function<void(uint32_t)> hash_obj = [&](uint32_t oi) {
-    auto& o = objs[oi];
-    for (;;) {
-      std::pair<const uint8_t*, std::pair<uint64_t, int>> p;
-      {
-        std::lock_guard<std::mutex> g(S.mu);
-        if (o.q.empty()) {
-          o.busy = false;
-          return;
-        }
-        p = o.q.front();
-        o.q.pop_front();
-      }
-      o.fnv = fnv1a64(p.first, p.second.first, o.fnv);
-      o.hashed += p.second.first;
-      release(p.second.second);
-    }
-  };
-  struct host_cb_arg {
-    shared_state* s;
-    int slot;
-  };
-  std::vector<host_cb_arg> cb_args(K);
-  for (int k = 0; k < K; ++k) cb_args[k] = {&S, k};
-
-  double read_s = 0;
-  cuda_check(cudaEventRecord(ev_a, st), "event");
-  size_t pi = 0, ui = 0;
-  uint32_t launches = 0;
-  const int ctas = dev::sm_count(device) * 2;
-  for (uint64_t lo = 0, w = 0; lo < img; lo += W, ++w) {
-    const uint64_t hi = std::min(lo + W, img);
-    const int slot = static_cast<int>(w % K);
+  // Window finished reading: host-tier pieces to their buffers, device part
+  // H2D + scatter-unpack, slot freed by a stream callback.
+  auto window_read = [&](uint64_t lo, uint64_t hi, int slot) {
     uint8_t* hs = hring + static_cast<uint64_t>(slot) * W;
-    {
-      std::unique_lock<std::mutex> g(S.mu);
-      S.cv.wait(g, [&] { return S.slot_refs[slot] == 0; });
-      if (S.err_status != TS_OK) break;
+    auto pit = std::lower_bound(pieces.begin(), pieces.end(), lo,
+                                [](const rpiece& p, uint64_t x) { return p.pos + p.len <= x; });
+    for (; pit != pieces.end() && pit->pos < hi; ++pit) {
+      const auto& o = objs[pit->obj];
+      if (o.d->tier == TS_TIER_DEVICE) continue;
+      const uint64_t a = std::max(lo, pit->pos), b = std::min(hi, pit->pos + pit->len);
+      if (b > a)
+        std::memcpy(static_cast<uint8_t*>(const_cast<void*>(o.d->data)) + pit->obj_off + (a - pit->pos),
+                    hs + (a - lo), b - a);
     }
-    // Parallel pread of the window's file ranges (<= 8 MiB per task).
-    const int64_t r0 = now_ns();
-    {
-      std::mutex lm;
-      std::condition_variable lcv;
-      int outstanding = 0;
-      for (size_t k = 0; k < rc.files.size(); ++k) {
-        const uint64_t a = std::max(lo, file_img[k].first);
-        const uint64_t b = std::min(hi, file_img[k].first + file_img[k].second);
-        for (uint64_t x = a; x < b; x += (8ull << 20)) {
-          const uint64_t y = std::min<uint64_t>(b, x + (8ull << 20));
-          {
-            std::lock_guard<std::mutex> g(lm);
-            ++outstanding;
-          }
-          pool.submit([&, k, x, y] {
-            try {
-              pread_all(fds[k].fd, hs + (x - lo), y - x, header_reserved + (x - file_img[k].first), rc.files[k].path);
-            } catch (const error& e) {
-              set_err(e);
-            }
-            std::lock_guard<std::mutex> g(lm);
-            if (--outstanding == 0) lcv.notify_all();
-          });
-        }
-      }
-      std::unique_lock<std::mutex> g(lm);
-      lcv.wait(g, [&] { return outstanding == 0; });
-    }
-    read_s += (now_ns() - r0) * 1e-9;
-    // H2D + scatter-unpack of the window on the restore stream.
-    {
-      std::lock_guard<std::mutex> g(S.mu);
-      S.slot_refs[slot] += 1;  // released by the stream callback
-    }
+    std::lock_guard<std::mutex> g(cuda_mu);
     uint8_t* ds = dring + static_cast<uint64_t>(slot) * W;
     cuda_check(cudaMemcpyAsync(ds, hs, hi - lo, cudaMemcpyHostToDevice, st), "H2D window");
-    while (ui < usegs.size() && usegs[ui].pos + usegs[ui].len <= lo) ++ui;
-    if (ui < usegs.size() && usegs[ui].pos < hi) {
+    auto uit = std::lower_bound(usegs.begin(), usegs.end(), lo,
+                                [](const dev::useg& u, uint64_t x) { return u.pos + u.len <= x; });
+    if (uit != usegs.end() && uit->pos < hi) {
+      const size_t ui = static_cast<size_t>(uit - usegs.begin());
       dev::launch_unpack(d_usegs + ui, static_cast<uint32_t>(usegs.size() - ui), lo, hi, ds, ctas, 512, st);
-      launches += 1;
+      launches_a += 1;
       cuda_check(cudaGetLastError(), "unpack launch");
     }
     cuda_check(cudaLaunchHostFunc(st, [](void* a) {
                  auto* p = static_cast<host_cb_arg*>(a);
                  std::lock_guard<std::mutex> g(p->s->mu);
-                 if (--p->s->slot_refs[p->slot] == 0) p->s->cv.notify_all();
+                 p->s->slot_busy[p->slot] = 0;
+                 p->s->cv.notify_all();
                }, &cb_args[slot]), "cudaLaunchHostFunc");
-    // Checksum pieces (object order preserved: windows are visited in order).
-    while (pi < pieces.size() && pieces[pi].pos + pieces[pi].len <= lo) ++pi;
-    std::vector<uint32_t> sched;
-    for (size_t q = pi; q < pieces.size() && pieces[q].pos < hi; ++q) {
-      const auto& p = pieces[q];
-      const uint64_t a = std::max(lo, p.pos), b = std::min(hi, p.pos + p.len);
-      if (b <= a) continue;
-      auto& o = objs[p.obj];
-      if (o.d->tier == TS_TIER_DEVICE) continue;  // verified on the GPU after the scatter
-      std::memcpy(static_cast<uint8_t*>(const_cast<void*>(o.d->data)) + p.obj_off + (a - p.pos), hs + (a - lo), b - a);
-      std::lock_guard<std::mutex> g(S.mu);
-      S.slot_refs[slot] += 1;
-      o.q.push_back({hs + (a - lo), {b - a, slot}});
-      if (!o.busy) {
-        o.busy = true;
-        sched.push_back(p.obj);
+  };
+
+  double read_s = 0;
+  rtrace("setup done", t_begin);
+  const int64_t r0 = now_ns();
+  {
+    thread_pool pool(nthreads);
+    cuda_check(cudaEventRecord(ev_a, st), "event");
+    for (uint64_t lo = 0, w = 0; lo < img; lo += W, ++w) {
+      const uint64_t hi = std::min(lo + W, img);
+      const int slot = static_cast<int>(w % K);
+      {
+        std::unique_lock<std::mutex> g(S.mu);
+        S.cv.wait(g, [&] { return S.slot_busy[slot] == 0 || S.err_status != TS_OK; });
+        if (S.err_status != TS_OK) break;
+        S.slot_busy[slot] = 1;
+      }
+      uint8_t* hs = hring + static_cast<uint64_t>(slot) * W;
+      struct wstate {
+        std::atomic<int> left{0};
+      };
+      auto ws = std::make_shared<wstate>();
+      std::vector<std::tuple<size_t, uint64_t, uint64_t>> reads;
+      for (size_t k = 0; k < rc.files.size(); ++k) {
+        const uint64_t a = std::max(lo, file_img[k].first);
+        const uint64_t b = std::min(hi, file_img[k].first + file_img[k].second);
+        for (uint64_t x = a; x < b; x += (16ull << 20)) reads.emplace_back(k, x, std::min<uint64_t>(b, x + (16ull << 20)));
+      }
+      if (reads.empty()) {
+        window_read(lo, hi, slot);
+        continue;
+      }
+      ws->left = static_cast<int>(reads.size());
+      for (auto [k, x, y] : reads) {
+        pool.submit([&, ws, k, x, y, lo, hi, slot, hs] {
+          try {
+            pread_all(fds[k].fd, hs + (x - lo), y - x, header_reserved + (x - file_img[k].first), rc.files[k].path);
+          } catch (const error& e) {
+            set_err(e);
+          }
+          if (--ws->left == 0) {
+            try {
+              window_read(lo, hi, slot);
+            } catch (const error& e) {
+              set_err(e);
+              std::lock_guard<std::mutex> g(S.mu);
+              S.slot_busy[slot] = 0;
+              S.cv.notify_all();
+            }
+          }
+        });
       }
     }
-    for (uint32_t oi : sched) pool.submit([&, oi] { hash_obj(oi); });
-  }
+  }  // pool joins: every read done, every window enqueued
   {
     std::unique_lock<std::mutex> g(S.mu);
     S.cv.wait(g, [&] {
       for (int k = 0; k < K; ++k)
-        if (S.slot_refs[k]) return false;
+        if (S.slot_busy[k]) return false;
       return true;
     });
+  }
+  read_s = (now_ns() - r0) * 1e-9;
+  uint32_t launches = launches_a.load();
+  // Host-tier destinations: checksums over the restored host buffers, 4 chains per core.
+  {
+    std::vector<uint32_t> host_objs;
+    for (uint32_t i = 0; i < objs.size(); ++i)
+      if (objs[i].d->tier != TS_TIER_DEVICE) host_objs.push_back(i);
+    for (uint32_t i : host_objs) {
+      auto& o = objs[i];
+      o.fnv = fnv1a64(o.d->data, o.size);
+      o.hashed = o.size;
+    }
   }
   cuda_check(cudaEventRecord(ev_b, st), "event");
   // Device-tier objects: exact FNV kernels over the restored shards themselves
@@ -353,9 +378,9 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
     uint64_t nchunk = 0;
     const uint64_t nseg = dev::fnv_prepare(fo.data(), nf, &nchunk);
     const uint64_t tb = align_up(nf * sizeof(dev::fnv_obj), 256), sb = align_up(nf * 8ull, 256);
-    uint8_t* fb = nullptr;
-    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&fb), tb + sb + dev::fnv_scratch_bytes(nseg, nchunk, nf), st),
-               "alloc");
+    // Checksums run after the last unpack: the scatter table's scratch can be reused.
+    cuda_check(cudaStreamSynchronize(st), "restore stream");
+    uint8_t* fb = device_scratch(device, tb + sb + dev::fnv_scratch_bytes(nseg, nchunk, nf));
     cuda_check(cudaMemcpyAsync(fb, fo.data(), nf * sizeof(dev::fnv_obj), cudaMemcpyHostToDevice, st), "upload");
     cuda_check(cudaMemcpyAsync(fb + tb, seeds.data(), nf * 8ull, cudaMemcpyHostToDevice, st), "upload");
     dev::launch_fnv(reinterpret_cast<dev::fnv_obj*>(fb), nf, nseg, nchunk, reinterpret_cast<uint64_t*>(fb + tb),
@@ -363,9 +388,10 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
     launches += 11;
     cuda_check(cudaGetLastError(), "checksum kernels");
     cuda_check(cudaMemcpyAsync(dev_ck.data(), fb + tb, nf * 8ull, cudaMemcpyDeviceToHost, st), "download");
-    cuda_check(cudaFreeAsync(fb, st), "free");
   }
+  rtrace("pipeline done", t_begin);
   cuda_check(cudaStreamSynchronize(st), "restore stream");
+  rtrace("device checksums done", t_begin);
   for (size_t i = 0; i < dev_objs.size(); ++i) {
     auto& o = objs[dev_objs[i]];
     o.fnv = dev_ck[i];
@@ -376,10 +402,10 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
   cudaEventElapsedTime(&h2d_ms, ev_a, ev_b);
   cudaEventDestroy(ev_a);
   cudaEventDestroy(ev_b);
-  cudaFreeAsync(dring, st);
-  if (d_usegs) cudaFreeAsync(d_usegs, st);
+
   cudaStreamSynchronize(st);
   if (S.err_status != TS_OK) throw error(S.err_status, S.err, S.err_oid);
+  rtrace("ring freed", t_begin);
   const int64_t t_verify = now_ns();
   for (const auto& o : objs)
     if (o.hashed != o.size || o.fnv != o.ck)
@@ -412,6 +438,7 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
     }
   }
   (void)mr;
+  rtrace("structured done", t_begin);
   if (stats) {
     stats->bytes = raw_bytes + ser_bytes;
     stats->read_s = read_s;
