@@ -209,7 +209,7 @@ def ours(args):
     cfg = api.EngineConfig(d2h_mode=args.mode, staging_capacity_bytes=pool, raw_chunk_bytes=64 << 20,
                            device_staging_bytes=img_est + (1 << 20) if shadow else int(args.ring_gb * (1 << 30)),
                            flush_workers=min(16, os.cpu_count() or 8), write_files=False,
-                           checksum_on_gpu=not args.host_checksum)
+                           checksum_on_gpu=not args.host_checksum, pack_kernel=args.pack_kernel)
     eng = api.CheckpointEngine(cfg, spec.rank_id, local)
     full = getattr(rec, "full_layout", None)
     echo = S.Recipe(layout=full).manifest_echo() if full else rec.manifest_echo()
@@ -351,7 +351,7 @@ def ours(args):
             "config": {"workload": f"{args.config}: {rec.name} rank-r shard, {len(spec.objects)} objects, "
                                    f"{bytes_step / 1e9:.3f} GB/rank", "d2h_mode": args.mode,
                        "device_shadow": bool(shadow), "pinned_pool_gb": round(pool / 2**30, 2),
-                       "checksums": "host" if args.host_checksum else "gpu", "l2": "inputs > L2 (126 MB)",
+                       "checksums": "host" if args.host_checksum else "gpu", "pack_kernel": args.pack_kernel, "l2": "inputs > L2 (126 MB)",
                        "step": "update(pattern kernel) + issue + snapshot + checksums (no files)"},
             "per_gpu_gbps": round(value / ws, 3),
             "snapshot_ms_mean": round(statistics.mean(snap_ms), 2),
@@ -433,6 +433,7 @@ def main():
     ap.add_argument("--fwd-bwd-ms", type=float, default=1800.0)
     ap.add_argument("--ckpt-interval", type=int, default=1, help="checkpoint every k training steps")
     ap.add_argument("--host-checksum", action="store_true", help="FNV on host threads instead of the GPU kernels")
+    ap.add_argument("--pack-kernel", default="warp", choices=["warp", "bulk"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pool-gb", type=float, default=0.0, help="pinned pool cap (default: image, at most 64 GiB)")
     ap.add_argument("--ring-gb", type=float, default=8.0, help="HBM staging ring when no full device shadow fits")

@@ -100,7 +100,8 @@ class EngineConfigC(C.Structure):
                 ("overwrite", C.c_int32), ("d2h_mode", C.c_int32), ("device_staging_bytes", C.c_uint64),
                 ("hybrid_direct_min_bytes", C.c_uint64), ("pack_ctas", C.c_int32),
                 ("pack_threads", C.c_int32), ("pack_priority", C.c_int32), ("write_files", C.c_int32),
-                ("checksum_on_gpu", C.c_int32), ("flush_mmap", C.c_int32)]
+                ("checksum_on_gpu", C.c_int32), ("flush_mmap", C.c_int32), ("pack_kernel", C.c_int32),
+                ("bulk_min_bytes", C.c_uint64)]
 
 
 class ManifestEcho(C.Structure):

@@ -256,6 +256,8 @@ class EngineConfig:
     write_files: bool = True
     checksum_on_gpu: bool = True
     flush_mmap: bool = True
+    pack_kernel: str = "warp"  # "warp" | "bulk" (TMA cp.async.bulk for large aligned fragments)
+    bulk_min_bytes: int = 1 << 20
 
     def to_c(self) -> N.EngineConfigC:
         c = N.EngineConfigC()
@@ -278,6 +280,8 @@ class EngineConfig:
         c.write_files = int(self.write_files)
         c.checksum_on_gpu = int(self.checksum_on_gpu)
         c.flush_mmap = int(self.flush_mmap)
+        c.pack_kernel = {"warp": 0, "bulk": 1}[self.pack_kernel]
+        c.bulk_min_bytes = self.bulk_min_bytes
         return c
 
 

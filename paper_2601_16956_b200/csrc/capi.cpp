@@ -195,6 +195,8 @@ void ts_engine_config_default(ts_engine_config* c) {
   c->write_files = 1;
   c->checksum_on_gpu = 1;
   c->flush_mmap = 1;
+  c->pack_kernel = 0;
+  c->bulk_min_bytes = 1ull << 20;
 }
 
 ts_status ts_engine_create(const ts_engine_config* cfg, int rank_id, int device, ts_engine** out) {

@@ -736,12 +736,44 @@ void engine::run_job(const std::shared_ptr<job>& j) {
   }
   const bool use_ring = ring != nullptr;
 
+  // TMA bulk jobs (pack_kernel = 1, RING only): large 16-B aligned device
+  // fragments are cut at absolute kBulkJob boundaries of the image (so no job
+  // straddles a ring chunk); the warp kernel skips those bytes.
+  std::vector<dev::seg> wsegs;
+  std::vector<dev::bulk_job> bjobs;
+  const std::vector<dev::seg>* segs_for_warp = &j->segs;
+  if (use_ring && cfg_.pack_kernel == 1) {
+    for (const auto& sg : j->segs) {
+      const uint64_t body = sg.len & ~15ull;
+      const bool bulk = sg.src && (reinterpret_cast<uintptr_t>(sg.src) & 15) == 0 && (sg.pos & 15) == 0 &&
+                        body >= std::max<uint64_t>(cfg_.bulk_min_bytes, dev::kBulkJob);
+      if (!bulk) {
+        wsegs.push_back(sg);
+        continue;
+      }
+      wsegs.push_back({sg.pos, body, TSB_BULK_SRC});
+      if (sg.len > body) wsegs.push_back({sg.pos + body, sg.len - body, sg.src + body});
+      for (uint64_t a = sg.pos; a < sg.pos + body;) {
+        const uint64_t b = std::min(sg.pos + body, (a / dev::kBulkJob + 1) * dev::kBulkJob);
+        bjobs.push_back({a, sg.src + (a - sg.pos), b - a});
+        a = b;
+      }
+    }
+    segs_for_warp = &wsegs;
+  }
   dev::seg* d_segs = nullptr;
+  dev::bulk_job* d_jobs = nullptr;
   if (j->img > 0 && mode != TS_D2H_DIRECT) {
-    d_segs = static_cast<dev::seg*>(ensure_seg_buffer(j->segs.size() * sizeof(dev::seg)));
+    const uint64_t sb = align_up(segs_for_warp->size() * sizeof(dev::seg), 256);
+    uint8_t* tb = static_cast<uint8_t*>(ensure_seg_buffer(sb + bjobs.size() * sizeof(dev::bulk_job)));
+    d_segs = reinterpret_cast<dev::seg*>(tb);
+    d_jobs = reinterpret_cast<dev::bulk_job*>(tb + sb);
     // Upload before waiting on the producer (a pageable H2D syncs its stream).
-    cuda_check(cudaMemcpyAsync(d_segs, j->segs.data(), j->segs.size() * sizeof(dev::seg),
+    cuda_check(cudaMemcpyAsync(d_segs, segs_for_warp->data(), segs_for_warp->size() * sizeof(dev::seg),
                                cudaMemcpyHostToDevice, pack_stream_), "upload segment table");
+    if (!bjobs.empty())
+      cuda_check(cudaMemcpyAsync(d_jobs, bjobs.data(), bjobs.size() * sizeof(dev::bulk_job), cudaMemcpyHostToDevice,
+                                 pack_stream_), "upload bulk jobs");
   }
   // Device checksums. RING: per chunk over the ring slot right after its pack
   // (chained states, off the capture path). DIRECT / ZEROCOPY: over the state
@@ -838,7 +870,7 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     mark_capture(pack_stream_);
     return;
   }
-  const uint32_t nsegs = static_cast<uint32_t>(j->segs.size());
+  const uint32_t nsegs = static_cast<uint32_t>(segs_for_warp->size());
 
   if (mode == TS_D2H_RING) {
     const bool shadow = nslots == 1;
@@ -854,9 +886,19 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       cuda_check(cudaEventCreate(&pb), "event");
       cuda_check(cudaEventRecord(pa, pack_stream_), "event");
       dev::launch_pack(d_segs, nsegs, clo, chi, slot, ctas, threads, pack_stream_);
+      t.kernel_launches += 1;
+      if (!bjobs.empty()) {
+        auto lb = std::lower_bound(bjobs.begin(), bjobs.end(), clo,
+                                   [](const dev::bulk_job& b, uint64_t x) { return b.pos < x; });
+        auto ub = std::lower_bound(lb, bjobs.end(), chi, [](const dev::bulk_job& b, uint64_t x) { return b.pos < x; });
+        if (ub > lb) {
+          dev::launch_pack_bulk(d_jobs + (lb - bjobs.begin()), static_cast<uint32_t>(ub - lb), clo, slot, sms_,
+                                pack_stream_);
+          t.kernel_launches += 1;
+        }
+      }
       cuda_check(cudaEventRecord(pb, pack_stream_), "event");
       j->pack_events.push_back({pa, pb});
-      t.kernel_launches += 1;
       cuda_check(cudaGetLastError(), "pack kernel launch");
       cudaEvent_t packed;
       cuda_check(cudaEventCreateWithFlags(&packed, cudaEventDisableTiming), "event");

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(512) pack_kernel(const seg* __restrict__ segs,
       const uint64_t pos = __ldg(&segs[k].pos), len = __ldg(&segs[k].len);
       const uint8_t* src = reinterpret_cast<const uint8_t*>(__ldg(reinterpret_cast<const unsigned long long*>(&segs[k].src)));
       const uint64_t e = min(b, pos + len);
-      if (e > a) warp_copy(dst + (a - lo), src ? src + (a - pos) : nullptr, e - a, lane);
+      if (e > a && src != TSB_BULK_SRC) warp_copy(dst + (a - lo), src ? src + (a - pos) : nullptr, e - a, lane);
       a = max(a, e);
       ++k;
     }
@@ -255,6 +255,59 @@ __global__ void __launch_bounds__(512) pattern_kernel(const pseg* __restrict__ s
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Bulk copy through shared memory with the TMA engine (cp.async.bulk).
+
+constexpr int kBulkStages = 6;  // 6 x 32 KiB = 192 KiB of shared memory per CTA
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__global__ void __launch_bounds__(32) pack_bulk_kernel(const bulk_job* __restrict__ jobs, uint32_t njobs,
+                                                       uint64_t lo, uint8_t* dst) {
+  extern __shared__ __align__(128) uint8_t stage_buf[];
+  __shared__ __align__(8) uint64_t bars[kBulkStages];
+  if (threadIdx.x != 0) return;
+  const uint32_t first = blockIdx.x, step = gridDim.x;
+  const uint32_t mine = first < njobs ? (njobs - first + step - 1) / step : 0;
+  if (mine == 0) return;
+  for (int s = 0; s < kBulkStages; ++s)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  auto issue = [&](uint32_t i) {
+    const bulk_job& jb = jobs[first + i * step];
+    const int s = static_cast<int>(i % kBulkStages);
+    const uint32_t bar = smem_u32(&bars[s]);
+    const uint32_t len = static_cast<uint32_t>(jb.len);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(len) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(stage_buf + s * kBulkJob)), "l"(jb.src), "r"(len), "r"(bar) : "memory");
+  };
+  for (uint32_t i = 0; i < mine && i < kBulkStages - 1; ++i) issue(i);
+  for (uint32_t i = 0; i < mine; ++i) {
+    const int s = static_cast<int>(i % kBulkStages);
+    const uint32_t bar = smem_u32(&bars[s]);
+    const uint32_t parity = (i / kBulkStages) & 1;
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    const bulk_job& jb = jobs[first + i * step];
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 ::"l"(dst + (jb.pos - lo)), "r"(smem_u32(stage_buf + s * kBulkJob)), "r"(static_cast<uint32_t>(jb.len))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    if (i + kBulkStages - 1 < mine) {
+      // stage (i-1) % S is reused: the store issued from it one step ago must have read it
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      issue(i + kBulkStages - 1);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int grid_for(uint64_t bytes, int ctas, int threads) {
   const uint64_t tiles = (bytes + kTileBytes - 1) / kTileBytes;
   const uint64_t warps_per_cta = static_cast<uint64_t>(threads / 32);
@@ -277,6 +330,20 @@ void launch_pack(const seg* d_segs, uint32_t nsegs, uint64_t lo, uint64_t hi, ui
                  int ctas, int threads, cudaStream_t st) {
   if (hi <= lo || nsegs == 0) return;
   pack_kernel<<<grid_for(hi - lo, ctas, threads), threads, 0, st>>>(d_segs, nsegs, lo, hi, dst);
+  count_launch();
+}
+
+void launch_pack_bulk(const bulk_job* d_jobs, uint32_t njobs, uint64_t lo, uint8_t* dst, int ctas,
+                      cudaStream_t st) {
+  if (njobs == 0) return;
+  static bool attr = false;
+  const int smem = kBulkStages * static_cast<int>(kBulkJob);
+  if (!attr) {
+    cudaFuncSetAttribute(pack_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  const int grid = static_cast<int>(std::min<uint64_t>(njobs, static_cast<uint64_t>(ctas)));
+  pack_bulk_kernel<<<grid, 32, smem, st>>>(d_jobs, njobs, lo, dst);
   count_launch();
 }
 

@@ -14,7 +14,9 @@
 
 namespace tsb::dev {
 
-// One piece of the image. src == nullptr => zero fill (alignment gaps).
+// One piece of the image. src == nullptr => zero fill (alignment gaps);
+// src == kBulkSrc => bytes written by the bulk-copy (TMA) kernel, skipped here.
+#define TSB_BULK_SRC (reinterpret_cast<const uint8_t*>(uintptr_t{1}))
 struct seg {
   uint64_t pos;  // virtual (image) offset
   uint64_t len;
@@ -44,6 +46,20 @@ constexpr uint32_t kTileBytes = 32768;  // virtual bytes per warp task
 // dst may be device memory (RING) or mapped pinned host memory (ZEROCOPY).
 void launch_pack(const seg* d_segs, uint32_t nsegs, uint64_t lo, uint64_t hi, uint8_t* dst,
                  int ctas, int threads, cudaStream_t st);
+
+// Bulk (TMA engine) copy jobs: dst image position, 16-B aligned source, length
+// a multiple of 16 and <= kBulkJob. One elected thread per CTA drives a ring of
+// shared-memory stages: cp.async.bulk global->shared completing on an
+// mbarrier, then cp.async.bulk shared->global, so SM issue slots stay free.
+constexpr uint32_t kBulkJob = 32768;
+struct bulk_job {
+  uint64_t pos;
+  const uint8_t* src;
+  uint64_t len;
+};
+// Copies jobs whose pos lies in [lo, hi) into dst (dst[0] = image byte lo).
+void launch_pack_bulk(const bulk_job* d_jobs, uint32_t njobs, uint64_t lo, uint8_t* dst, int ctas,
+                      cudaStream_t st);
 
 // Scatter-unpack: image bytes [lo, hi) held in src (src[0] = image byte lo)
 // to the destination pieces that intersect the range.

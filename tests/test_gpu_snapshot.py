@@ -16,12 +16,15 @@ from paper_2601_16956_b200 import api
 from paper_2601_16956_b200 import synthetic as S
 
 pytestmark = pytest.mark.gpu
-MODES = ["ring", "direct", "zerocopy"]
+MODES = ["ring", "direct", "zerocopy", "ring-bulk"]
 
 
 def cfg_for(mode, **kw):
+    extra = {}
+    if mode == "ring-bulk":  # TMA bulk copies for every fragment >= 32 KiB
+        mode, extra = "ring", dict(pack_kernel="bulk", bulk_min_bytes=32768)
     base = dict(d2h_mode=mode, raw_chunk_bytes=64 << 10, staging_capacity_bytes=1 << 20,
-                device_staging_bytes=256 << 10, flush_workers=3)
+                device_staging_bytes=256 << 10, flush_workers=3, **extra)
     base.update(kw)
     return api.EngineConfig(**base)
 
