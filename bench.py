@@ -208,7 +208,7 @@ def ours(args):
     pool = (min(img_est + (64 << 20), pool_cap) + (2 << 20) - 1) // (2 << 20) * (2 << 20)
     cfg = api.EngineConfig(d2h_mode=args.mode, staging_capacity_bytes=pool, raw_chunk_bytes=64 << 20,
                            device_staging_bytes=img_est + (1 << 20) if shadow else int(args.ring_gb * (1 << 30)),
-                           flush_workers=min(16, os.cpu_count() or 8), write_files=False,
+                           flush_workers=args.flush_workers or min(16, os.cpu_count() or 8), write_files=False,
                            checksum_on_gpu=not args.host_checksum, pack_kernel=args.pack_kernel)
     eng = api.CheckpointEngine(cfg, spec.rank_id, local)
     full = getattr(rec, "full_layout", None)
@@ -281,15 +281,25 @@ def ours(args):
         cfg_io = api.EngineConfig(**{**cfg.__dict__, "write_files": True})
         eng.shutdown()
         eng_io = api.CheckpointEngine(cfg_io, spec.rank_id, local)
-        step(it + 1, eng_io, True)  # warm the file path
-        it += 1
+        for _ in range(2):  # warm the file path (and, with rotation, fill the retention window)
+            it += 1
+            step(it, eng_io, True)
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
-        for _ in range(args.e2e_steps):  # checkpoints are deleted after the timed region
+        spare = os.path.join(tdir, ".spare")
+        if not args.fresh_files:
+            eng_io.set_spare_dir(spare)
+        for _ in range(args.e2e_steps):
             it += 1
+            # rotation: keep the last 2 checkpoints, recycle older files
+            old = os.path.join(tdir, f"ckpt_{it - 2:06d}")
+            if not args.fresh_files and rank == 0 and os.path.exists(old):
+                api.retire_checkpoint(old, spare)
+            if ws > 1:
+                dist.barrier()
             st, sess = step(it, eng_io, True)
         f1.record()
         torch.cuda.synchronize()
@@ -302,7 +312,8 @@ def ours(args):
                "persist_ms_last": round(st["t_persisted_ns"] / 1e6, 1),
                "snapshot_ms_last": round(st["t_snapshot_ns"] / 1e6, 1),
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(image),
-               "what": "issue -> files + footers + MANIFEST.tlv durable on /dev/shm, via the C-ABI"}
+               "what": "issue -> files + footers + MANIFEST.tlv durable on /dev/shm, via the C-ABI"
+                       + ("" if args.fresh_files else "; rotation keeps 2 checkpoints, older files recycled")}
         # restore of the last checkpoint (H2D + scatter-unpack + FNV verify)
         man = os.path.join(tdir, f"ckpt_{it:06d}", "MANIFEST.tlv")
         r = api.Restorer(man)
@@ -434,6 +445,9 @@ def main():
     ap.add_argument("--ckpt-interval", type=int, default=1, help="checkpoint every k training steps")
     ap.add_argument("--host-checksum", action="store_true", help="FNV on host threads instead of the GPU kernels")
     ap.add_argument("--pack-kernel", default="warp", choices=["warp", "bulk"])
+    ap.add_argument("--flush-workers", type=int, default=0, help="host worker threads (default: min(16, cores))")
+    ap.add_argument("--fresh-files", action="store_true",
+                    help="e2e: new files every checkpoint (no rotation / recycling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pool-gb", type=float, default=0.0, help="pinned pool cap (default: image, at most 64 GiB)")
     ap.add_argument("--ring-gb", type=float, default=8.0, help="HBM staging ring when no full device shadow fits")

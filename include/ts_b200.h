@@ -196,6 +196,14 @@ typedef struct ts_manifest_echo {
   uint64_t metadata_bytes;
 } ts_manifest_echo;
 
+/* Checkpoint rotation (B200 addition; the reference never deletes): retire a
+ * checkpoint directory (MANIFEST.tlv removed first, so it is no longer
+ * restorable) and move its rank files to `spare_dir`; an engine given the same
+ * spare directory takes those files over for its next checkpoints instead of
+ * allocating fresh page-cache pages. Same filesystem required. */
+ts_status ts_retire_checkpoint(const char* ckpt_dir, const char* spare_dir);
+ts_status ts_engine_set_spare_dir(ts_engine* e, const char* spare_dir);
+
 /* checkpoint_session (engine.hpp:57-90). `writes_manifest` = 1 on the process that
  * commits MANIFEST.tlv once all n_ranks ranks persisted (local or remote). */
 ts_status ts_session_create(const char* dir, uint64_t checkpoint_id, uint64_t iteration,

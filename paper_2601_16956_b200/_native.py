@@ -184,6 +184,8 @@ _sig("ts_fnv1a64", u64, P, sz, u64)
 _sig("ts_engine_config_default", None, C.POINTER(EngineConfigC))
 _sig("ts_engine_create", i32, C.POINTER(EngineConfigC), i32, i32, C.POINTER(P))
 _sig("ts_engine_destroy", i32, P)
+_sig("ts_retire_checkpoint", i32, C.c_char_p, C.c_char_p)
+_sig("ts_engine_set_spare_dir", i32, P, C.c_char_p)
 _sig("ts_session_create", i32, C.c_char_p, u64, u64, C.POINTER(ManifestEcho), i32, i32, C.POINTER(P))
 _sig("ts_session_destroy", i32, P)
 _sig("ts_session_rank_blob", i32, P, i32, P, sz, C.POINTER(sz))

@@ -442,6 +442,10 @@ class CheckpointEngine:
         N.call(N.lib.ts_pre_update_barrier, self.h, ticket.h, C.c_void_p(sh), host_block, C.byref(ns))
         return ns.value
 
+    def set_spare_dir(self, spare_dir: str):
+        """Take over files of checkpoints retired into `spare_dir` (retire_checkpoint)."""
+        N.call(N.lib.ts_engine_set_spare_dir, self.h, spare_dir.encode())
+
     def shutdown(self):
         if self.h:
             N.call(N.lib.ts_engine_destroy, self.h)
@@ -549,6 +553,12 @@ class VerifyReport:
     files_checked: int
     objects_checked: int
     issues: List[tuple]
+
+
+def retire_checkpoint(ckpt_dir: str, spare_dir: str):
+    """Checkpoint rotation: invalidate `ckpt_dir` (manifest first) and move its files
+    to `spare_dir` for reuse by engines with set_spare_dir(spare_dir)."""
+    N.call(N.lib.ts_retire_checkpoint, ckpt_dir.encode(), spare_dir.encode())
 
 
 def verify_checkpoint(manifest_path: str) -> VerifyReport:

@@ -215,6 +215,14 @@ ts_status ts_engine_create(const ts_engine_config* cfg, int rank_id, int device,
   });
 }
 
+ts_status ts_retire_checkpoint(const char* ckpt_dir, const char* spare_dir) {
+  return guard([&] { retire_checkpoint(ckpt_dir, spare_dir); });
+}
+
+ts_status ts_engine_set_spare_dir(ts_engine* e, const char* spare_dir) {
+  return guard([&] { e->e->set_spare_dir(spare_dir ? spare_dir : ""); });
+}
+
 ts_status ts_engine_destroy(ts_engine* e) {
   return guard([&] { delete e; });
 }

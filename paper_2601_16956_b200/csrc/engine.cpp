@@ -474,9 +474,11 @@ std::shared_ptr<ticket_state> engine::issue(session& s, const ts_rank_info& rank
     cursor = align_up(cursor, 4096);
     fs.img = cursor;
     cursor += fp.tensor_region_end - header_reserved;
-    fs.w = std::make_unique<file_writer>(rdir + "/file_" + std::to_string(fp.file_id) + ".bin",
-                                         fp.tensor_region_end, j->plan.hash, cfg_.overwrite != 0,
-                                         j->io);
+    const std::string fname = "file_" + std::to_string(fp.file_id) + ".bin";
+    const std::string recycled =
+        spare_dir_.empty() ? std::string() : spare_dir_ + "/" + rank_dir_name(rank.rank_id) + "_" + fname;
+    fs.w = std::make_unique<file_writer>(rdir + "/" + fname, fp.tensor_region_end, j->plan.hash,
+                                         cfg_.overwrite != 0, j->io, recycled);
     fs.append_end = fp.tensor_region_end;
     if (cfg_.flush_mmap) fs.w->map_fixed_region();
     fidx.emplace(fp.file_id, static_cast<uint32_t>(j->files.size()));

@@ -119,6 +119,7 @@ class engine {
   int64_t pre_update_barrier(const std::shared_ptr<ticket_state>& t, cudaStream_t opt_stream,
                              int host_block);
   void shutdown();
+  void set_spare_dir(const std::string& d) { spare_dir_ = d; }
   const ts_engine_config& config() const { return cfg_; }
   int device() const { return device_; }
 
@@ -169,6 +170,7 @@ class engine {
   std::deque<pending_window> inflight_;
   bool stopping_ = false, copier_done_ = false;
   std::shared_ptr<job> last_job_;
+  std::string spare_dir_;  // recycled files of retired checkpoints (retire_checkpoint)
   std::thread copier_, completer_;
 };
 

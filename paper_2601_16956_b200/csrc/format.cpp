@@ -7,6 +7,8 @@
 #include <sys/statvfs.h>
 #include <unistd.h>
 
+#include <dirent.h>
+
 #include <algorithm>
 #include <cerrno>
 #include <cstdio>
@@ -157,11 +159,15 @@ void pread_all(int fd, void* p, size_t n, uint64_t off, const std::string& path)
 
 // format.cpp:125-147: header block, pre-size to tensor_region_end.
 file_writer::file_writer(const std::string& path, uint64_t tre, uint64_t plan_hash, bool overwrite,
-                         bool io)
+                         bool io, const std::string& recycled)
     : path_(path), tre_(tre), io_(io) {
   if (!io_) return;
   if (!overwrite && ::access(path.c_str(), F_OK) == 0) fail(TS_ERR_IO, "file exists: " + path);
-  fd_ = ::open(path.c_str(), O_RDWR | O_CREAT | O_TRUNC, 0644);
+  if (!recycled.empty() && ::rename(recycled.c_str(), path.c_str()) == 0) {
+    fd_ = ::open(path.c_str(), O_RDWR);
+    reused_ = fd_ >= 0;
+  }
+  if (fd_ < 0) fd_ = ::open(path.c_str(), O_RDWR | O_CREAT | O_TRUNC, 0644);
   if (fd_ < 0) fail(TS_ERR_IO, "cannot create " + path + ": " + std::strerror(errno));
   uint8_t header[header_reserved] = {};
   std::memcpy(header, "TSCKPT01", 8);
@@ -188,6 +194,7 @@ void file_writer::map_fixed_region() {
   // only map when the space is there, else keep positional writes.
   struct statvfs vs;
   if (::fstatvfs(fd_, &vs) != 0 || static_cast<uint64_t>(vs.f_bavail) * vs.f_frsize < tre_ + (64ull << 20)) return;
+  // (a recycled file's pages exist: its faults only map them)
   void* m = ::mmap(nullptr, tre_, PROT_READ | PROT_WRITE, MAP_SHARED, fd_, 0);
   if (m == MAP_FAILED) return;  // fall back to positional writes
   map_ = static_cast<uint8_t*>(m);
@@ -282,6 +289,34 @@ std::vector<footer_entry> read_footer(const std::string& path, uint64_t* file_si
     out[i] = {get_u64(e), e[8], get_u64(e + 9), get_u64(e + 17), get_u64(e + 25), get_u64(e + 33)};
   }
   return out;
+}
+
+void retire_checkpoint(const std::string& dir, const std::string& spare_dir) {
+  ::mkdir(spare_dir.c_str(), 0755);
+  if (::unlink((dir + "/MANIFEST.tlv").c_str()) != 0 && errno != ENOENT)
+    fail(TS_ERR_IO, "cannot retire " + dir + ": " + std::strerror(errno));
+  DIR* d = ::opendir(dir.c_str());
+  if (!d) fail(TS_ERR_MISSING_FILE, "cannot open " + dir);
+  std::vector<std::string> ranks;
+  while (dirent* e = ::readdir(d))
+    if (std::strncmp(e->d_name, "rank_", 5) == 0) ranks.push_back(e->d_name);
+  ::closedir(d);
+  for (const auto& r : ranks) {
+    const std::string rd = dir + "/" + r;
+    DIR* rdh = ::opendir(rd.c_str());
+    if (!rdh) continue;
+    std::vector<std::string> files;
+    while (dirent* e = ::readdir(rdh))
+      if (std::strncmp(e->d_name, "file_", 5) == 0) files.push_back(e->d_name);
+    ::closedir(rdh);
+    for (const auto& f : files) {
+      const std::string dst = spare_dir + "/" + r + "_" + f;
+      if (::rename((rd + "/" + f).c_str(), dst.c_str()) != 0)
+        fail(TS_ERR_IO, "cannot recycle " + rd + "/" + f + ": " + std::strerror(errno));
+    }
+    ::rmdir(rd.c_str());
+  }
+  ::rmdir(dir.c_str());
 }
 
 // ---------------------------------------------------------------------------

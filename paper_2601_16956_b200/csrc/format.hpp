@@ -51,8 +51,12 @@ void validate_entries(const std::vector<footer_entry>& entries, uint64_t tensor_
 // offsets, footer at finalize (format.cpp:125-199).
 class file_writer {
  public:
+  // `recycled`: a file of a retired checkpoint to take over (rename) instead of
+  // creating a fresh one: its page-cache pages are reused, every byte the
+  // checkpoint needs is rewritten (header, whole fixed region incl. zero gaps,
+  // appends, footer; the old tail is truncated away).
   file_writer(const std::string& path, uint64_t tensor_region_end, uint64_t plan_hash,
-              bool overwrite, bool io);
+              bool overwrite, bool io, const std::string& recycled = "");
   ~file_writer();
   void write_at(uint64_t off, const void* p, size_t n);
   // Fixed-region writes through a shared mapping of [0, tensor_region_end):
@@ -76,8 +80,15 @@ class file_writer {
   int fd_ = -1;
   uint64_t tre_;
   bool io_;
+  bool reused_ = false;
   uint8_t* map_ = nullptr;
 };
+
+// Retires a checkpoint (MANIFEST.tlv removed first, so it is no longer
+// restorable) and moves its rank files into `spare_dir` for reuse by later
+// checkpoints (see file_writer's `recycled`). Checkpoint rotation without
+// freeing and re-faulting the page cache.
+void retire_checkpoint(const std::string& dir, const std::string& spare_dir);
 
 struct file_header {
   uint32_t version;

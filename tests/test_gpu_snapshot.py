@@ -162,3 +162,46 @@ def test_back_pressure_bounded_pool(gpu, tmp_path):
     out = str(tmp_path / "bp")
     checkpoint_recipe(rec, out, cfg_for("direct", staging_capacity_bytes=8192, raw_chunk_bytes=8192))
     assert read_tree(out) == read_tree(os.path.join(GOLDEN, "trees", name))
+
+
+@pytest.mark.parametrize("name", ["hand_mixed", "odd_layout", "zero3_tiny"])
+def test_rotation_reuses_files_byte_identical(gpu, tmp_path, name):
+    """Checkpoint rotation: a checkpoint written over files recycled from a
+    retired, different checkpoint (other iteration, other layout: larger and
+    smaller files) is byte-identical to the reference's."""
+    rec = S.load_recipe(os.path.join(GOLDEN, "recipes", name + ".recipe"))
+    other = S.load_recipe(os.path.join(GOLDEN, "recipes", "tiny_layout.recipe"))
+    spare = str(tmp_path / "spare")
+    # an unrelated checkpoint of the same rank ids to recycle
+    for r, o in zip(rec.ranks, other.ranks):
+        o.rank_id = r.rank_id
+    other.ranks = other.ranks[:len(rec.ranks)]
+    old = str(tmp_path / "old")
+    checkpoint_recipe(other, old, cfg_for("ring"))
+    api.retire_checkpoint(old, spare)
+    assert not os.path.exists(old)
+    assert len(os.listdir(spare)) > 0
+    session = api.CheckpointSession(str(tmp_path / "new"), rec.ckpt_id, rec.iteration, rec.manifest_echo(),
+                                    n_ranks=len(rec.ranks))
+    states = [api.materialize_payloads(r, 0, rec.pit) for r in rec.ranks]
+    engines = [api.CheckpointEngine(cfg_for("ring"), r.rank_id, 0) for r in rec.ranks]
+    for e in engines:
+        e.set_spare_dir(spare)
+    tickets = [e.issue_checkpoint(session, s, rec.iteration) for e, s in zip(engines, states)]
+    for t in tickets:
+        t.wait_persisted()
+    session.wait_complete(60)
+    for e in engines:
+        e.shutdown()
+    assert read_tree(str(tmp_path / "new")) == read_tree(os.path.join(GOLDEN, "trees", name))
+
+
+def test_retired_checkpoint_is_not_restorable(gpu, tmp_path):
+    rec = S.load_recipe(os.path.join(GOLDEN, "recipes", "two_ranks.recipe"))
+    d = str(tmp_path / "c")
+    checkpoint_recipe(rec, d, cfg_for("ring"))
+    assert api.verify_checkpoint(os.path.join(d, "MANIFEST.tlv")).ok
+    api.retire_checkpoint(d, str(tmp_path / "spare"))
+    with pytest.raises(api.FormatError) as ei:
+        api.restore_checkpoint(os.path.join(d, "MANIFEST.tlv"))
+    assert ei.value.kind == "missing_file"
