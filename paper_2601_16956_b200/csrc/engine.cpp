@@ -744,7 +744,9 @@ void engine::run_job(const std::shared_ptr<job>& j) {
   std::vector<dev::seg> wsegs;
   std::vector<dev::bulk_job> bjobs;
   const std::vector<dev::seg>* segs_for_warp = &j->segs;
-  if (use_ring && cfg_.pack_kernel == 1) {
+  // (chunks must be kBulkJob multiples so that no job straddles two ring slots;
+  // with odd window sizes the warp kernel does everything)
+  if (use_ring && cfg_.pack_kernel == 1 && chunk % dev::kBulkJob == 0) {
     for (const auto& sg : j->segs) {
       const uint64_t body = sg.len & ~15ull;
       const bool bulk = sg.src && (reinterpret_cast<uintptr_t>(sg.src) & 15) == 0 && (sg.pos & 15) == 0 &&

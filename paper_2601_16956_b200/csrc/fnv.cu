@@ -70,8 +70,9 @@ struct seg_ref {
 __device__ __forceinline__ seg_ref seg_of(const fnv_obj* o, uint32_t n, uint64_t g, uint32_t* obj) {
   const uint32_t i = fnv_obj_of(o, n, g);
   *obj = i;
-  const uint64_t off = (g - o[i].seg0) * kFnvSeg;
-  return {o[i].ptr + off, umin64(kFnvSeg, o[i].len - off)};
+  const uint64_t sl = o[i].seglen;
+  const uint64_t off = (g - o[i].seg0) * sl;
+  return {o[i].ptr + off, umin64(sl, o[i].len - off)};
 }
 
 // Pass A: end low nibble for each of the 16 possible start low nibbles.
@@ -96,7 +97,12 @@ __global__ void __launch_bounds__(256) fnv_pass_a(const fnv_obj* __restrict__ o,
   piA[g] = m;
 }
 
-// Pass B: with the start low nibble fixed, end high nibble for the 16 start high nibbles.
+// Pass B: with the start low nibble fixed, end high nibble for the 16 start
+// high nibbles. With x = l ^ b = 16*xh + xl and t = xl * 0xb3 (known once the
+// low-nibble trajectory is), the byte update splits into
+//     lo' = t mod 16,   hi' = (3*xh + (t >> 4)) mod 16,
+// i.e. 4-bit lanes: 16 candidates in four 32-bit registers, one LOP3 + one
+// IMAD per register per byte (no 16-bit lanes, no multiply by 0xb3 per lane).
 __global__ void __launch_bounds__(256) fnv_pass_b(const fnv_obj* __restrict__ o, uint32_t n, uint64_t nseg,
                                                   const uint8_t* __restrict__ lo_start,
                                                   uint64_t* __restrict__ piB) {
@@ -104,21 +110,22 @@ __global__ void __launch_bounds__(256) fnv_pass_b(const fnv_obj* __restrict__ o,
   if (g >= nseg) return;
   uint32_t obj;
   const seg_ref s = seg_of(o, n, g, &obj);
-  const uint32_t lo = lo_start[g];
-  uint32_t w[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) w[j] = (((2u * j) << 4) | lo) | ((((2u * j + 1) << 4) | lo) << 16);
+  uint32_t lo = lo_start[g];
+  uint32_t v0 = 0x03020100u, v1 = 0x07060504u, v2 = 0x0b0a0908u, v3 = 0x0f0e0d0cu;
   for_bytes(s.p, s.len, [&](uint32_t b) {
-    const uint32_t bb = b * 0x00010001u;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) w[j] = ((w[j] ^ bb) * 0xb3u) & 0x00ff00ffu;
+    const uint32_t t = ((lo ^ b) & 15u) * 0xb3u;
+    lo = t & 15u;
+    const uint32_t c = ((t >> 4) & 15u) * 0x01010101u;
+    const uint32_t bh = (b >> 4) * 0x01010101u;
+    v0 = (((v0 ^ bh) * 3u) + c) & 0x0f0f0f0fu;
+    v1 = (((v1 ^ bh) * 3u) + c) & 0x0f0f0f0fu;
+    v2 = (((v2 ^ bh) * 3u) + c) & 0x0f0f0f0fu;
+    v3 = (((v3 ^ bh) * 3u) + c) & 0x0f0f0f0fu;
   });
+  const uint32_t v[4] = {v0, v1, v2, v3};
   uint64_t m = 0;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    m |= static_cast<uint64_t>((w[j] >> 4) & 15u) << (4 * (2 * j));
-    m |= static_cast<uint64_t>((w[j] >> 20) & 15u) << (4 * (2 * j + 1));
-  }
+  for (int s4 = 0; s4 < 16; ++s4) m |= static_cast<uint64_t>((v[s4 >> 2] >> (8 * (s4 & 3))) & 15u) << (4 * s4);
   piB[g] = m;
 }
 
@@ -159,7 +166,7 @@ __device__ __forceinline__ uint64_t nib_compose(uint64_t m, uint64_t p) {
   return r;
 }
 
-__device__ __forceinline__ uint64_t obj_nseg(const fnv_obj& o) { return (o.len + kFnvSeg - 1) / kFnvSeg; }
+__device__ __forceinline__ uint64_t obj_nseg(const fnv_obj& o) { return (o.len + o.seglen - 1) / o.seglen; }
 
 // chunk c of the global chunk space -> (object, first segment, segment count)
 struct chunk_ref {
@@ -238,13 +245,14 @@ __global__ void fnv_chunk_affine(const fnv_obj* __restrict__ o, uint32_t n,
   const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c >= nchunk) return;
   const chunk_ref r = chunk_of(o, n, c);
-  const uint64_t pk = pow_p(kFnvSeg);
+  const fnv_obj& ob0 = o[r.obj];
+  const uint64_t pk = pow_p(ob0.seglen);
   uint64_t a = 1, cv = 0;
   const fnv_obj& ob = o[r.obj];
   for (uint64_t s = 0; s < r.n; ++s) {
     const uint64_t g = r.g0 + s;
-    const uint64_t len = umin64(kFnvSeg, ob.len - (g - ob.seg0) * kFnvSeg);
-    const uint64_t m = len == kFnvSeg ? pk : pow_p(len);
+    const uint64_t len = umin64(ob.seglen, ob.len - (g - ob.seg0) * ob.seglen);
+    const uint64_t m = len == ob.seglen ? pk : pow_p(len);
     a = (m * a) & kM56;
     cv = (m * cv + cseg[g]) & kM56;
   }
@@ -278,11 +286,18 @@ uint64_t fnv_scratch_bytes(uint64_t nseg, uint64_t nchunk, uint32_t nobj) {
 }
 
 uint64_t fnv_prepare(fnv_obj* objs, uint32_t n, uint64_t* nchunk) {
+  // Segment length: 16 KiB, shrunk (to >= 1 KiB) until the launch has about two
+  // waves of threads, so many small fragments still fill the GPU.
+  uint64_t total = 0;
+  for (uint32_t i = 0; i < n; ++i) total += objs[i].len;
+  uint64_t seglen = kFnvSeg;
+  while (seglen > 1024 && total / seglen < 600000) seglen >>= 1;
   uint64_t g = 0, c = 0;
   for (uint32_t i = 0; i < n; ++i) {
-    const uint64_t ns = (objs[i].len + kFnvSeg - 1) / kFnvSeg;
+    const uint64_t ns = (objs[i].len + seglen - 1) / seglen;
     objs[i].seg0 = g;
     objs[i].chunk0 = c;
+    objs[i].seglen = seglen;
     g += ns;
     c += (ns + kChunk - 1) / kChunk;
   }

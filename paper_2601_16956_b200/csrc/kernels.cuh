@@ -83,6 +83,7 @@ struct fnv_obj {
   uint64_t chunk0;  // first global chunk index (chunks of 64 segments, per object)
   uint64_t sidx;    // index of this range's chain state in d_states / out (pieces of one
                     // object in later launches continue from the same state)
+  uint64_t seglen;  // segment length of the launch (set by fnv_prepare, <= kFnvSeg)
 };
 inline uint64_t align_up_dev(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 // Fills seg0/chunk0 of a host table; returns the segment count, *nchunk the chunk count.
