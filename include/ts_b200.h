@@ -177,6 +177,12 @@ typedef struct ts_engine_config {
                                        for 16-B aligned fragments >= bulk_min_bytes, warp kernel
                                        for the rest */
   uint64_t bulk_min_bytes;          /* default 1 MiB */
+  int32_t file_dma;                 /* 1 (default): D2H windows land directly in page-locked
+                                       file pages (cudaHostRegister of a shared mapping, tmpfs)
+                                       when a registration of the file exists; with a spare
+                                       directory set, finalized files are registered in the
+                                       background for reuse by rotation. 0: always pool + flush */
+  int32_t _pad1;
 } ts_engine_config;
 
 void ts_engine_config_default(ts_engine_config* cfg);
@@ -203,6 +209,11 @@ typedef struct ts_manifest_echo {
  * allocating fresh page-cache pages. Same filesystem required. */
 ts_status ts_retire_checkpoint(const char* ckpt_dir, const char* spare_dir);
 ts_status ts_engine_set_spare_dir(ts_engine* e, const char* spare_dir);
+/* Page-locked checkpoint files (ts_engine_config.file_dma): bytes currently
+ * locked, and an explicit release of every idle registration (files of deleted
+ * checkpoints are also released at the next issue). */
+uint64_t ts_file_cache_bytes(void);
+ts_status ts_file_cache_release_all(uint64_t* released_bytes);
 
 /* checkpoint_session (engine.hpp:57-90). `writes_manifest` = 1 on the process that
  * commits MANIFEST.tlv once all n_ranks ranks persisted (local or remote). */
@@ -249,6 +260,7 @@ typedef struct ts_ticket_stats {
   float d2h_ms;    /* CUDA-event time from first to last D2H window */
   uint32_t kernel_launches, copies;
   int32_t snapshot_done, persisted_done, failed;
+  uint64_t file_dma_bytes; /* fixed-region bytes the copy engines wrote straight into file pages */
 } ts_ticket_stats;
 ts_status ts_ticket_stats_get(ts_ticket* t, ts_ticket_stats* out);
 /* Per-object checksum accumulated at staging (transfer.cpp:163-166) */

@@ -101,7 +101,7 @@ class EngineConfigC(C.Structure):
                 ("hybrid_direct_min_bytes", C.c_uint64), ("pack_ctas", C.c_int32),
                 ("pack_threads", C.c_int32), ("pack_priority", C.c_int32), ("write_files", C.c_int32),
                 ("checksum_on_gpu", C.c_int32), ("flush_mmap", C.c_int32), ("pack_kernel", C.c_int32),
-                ("bulk_min_bytes", C.c_uint64)]
+                ("bulk_min_bytes", C.c_uint64), ("file_dma", C.c_int32), ("_pad1", C.c_int32)]
 
 
 class ManifestEcho(C.Structure):
@@ -117,7 +117,7 @@ class TicketStats(C.Structure):
                 ("t_captured_ns", C.c_int64), ("t_snapshot_ns", C.c_int64), ("t_persisted_ns", C.c_int64),
                 ("pack_ms", C.c_float), ("d2h_ms", C.c_float), ("kernel_launches", C.c_uint32),
                 ("copies", C.c_uint32), ("snapshot_done", C.c_int32), ("persisted_done", C.c_int32),
-                ("failed", C.c_int32)]
+                ("failed", C.c_int32), ("file_dma_bytes", C.c_uint64)]
 
 
 class RestoreObject(C.Structure):
@@ -186,6 +186,8 @@ _sig("ts_engine_create", i32, C.POINTER(EngineConfigC), i32, i32, C.POINTER(P))
 _sig("ts_engine_destroy", i32, P)
 _sig("ts_retire_checkpoint", i32, C.c_char_p, C.c_char_p)
 _sig("ts_engine_set_spare_dir", i32, P, C.c_char_p)
+_sig("ts_file_cache_bytes", C.c_uint64)
+_sig("ts_file_cache_release_all", i32, C.POINTER(C.c_uint64))
 _sig("ts_session_create", i32, C.c_char_p, u64, u64, C.POINTER(ManifestEcho), i32, i32, C.POINTER(P))
 _sig("ts_session_destroy", i32, P)
 _sig("ts_session_rank_blob", i32, P, i32, P, sz, C.POINTER(sz))

@@ -258,6 +258,7 @@ class EngineConfig:
     flush_mmap: bool = True
     pack_kernel: str = "warp"  # "warp" | "bulk" (TMA cp.async.bulk for large aligned fragments)
     bulk_min_bytes: int = 1 << 20
+    file_dma: bool = True  # D2H straight into page-locked file pages when registered (rotation)
 
     def to_c(self) -> N.EngineConfigC:
         c = N.EngineConfigC()
@@ -282,6 +283,7 @@ class EngineConfig:
         c.flush_mmap = int(self.flush_mmap)
         c.pack_kernel = {"warp": 0, "bulk": 1}[self.pack_kernel]
         c.bulk_min_bytes = self.bulk_min_bytes
+        c.file_dma = int(self.file_dma)
         return c
 
 
@@ -553,6 +555,18 @@ class VerifyReport:
     files_checked: int
     objects_checked: int
     issues: List[tuple]
+
+
+def file_cache_bytes() -> int:
+    """Bytes of checkpoint-file pages currently page-locked for direct D2H."""
+    return int(N.lib.ts_file_cache_bytes())
+
+
+def file_cache_release_all() -> int:
+    """Unlock every idle page-locked checkpoint file; returns the bytes released."""
+    b = C.c_uint64(0)
+    N.call(N.lib.ts_file_cache_release_all, C.byref(b))
+    return int(b.value)
 
 
 def retire_checkpoint(ckpt_dir: str, spare_dir: str):

@@ -197,6 +197,7 @@ void ts_engine_config_default(ts_engine_config* c) {
   c->flush_mmap = 1;
   c->pack_kernel = 0;
   c->bulk_min_bytes = 1ull << 20;
+  c->file_dma = 1;
 }
 
 ts_status ts_engine_create(const ts_engine_config* cfg, int rank_id, int device, ts_engine** out) {
@@ -221,6 +222,15 @@ ts_status ts_retire_checkpoint(const char* ckpt_dir, const char* spare_dir) {
 
 ts_status ts_engine_set_spare_dir(ts_engine* e, const char* spare_dir) {
   return guard([&] { e->e->set_spare_dir(spare_dir ? spare_dir : ""); });
+}
+
+uint64_t ts_file_cache_bytes(void) { return file_registry::get().registered_bytes(); }
+
+ts_status ts_file_cache_release_all(uint64_t* released_bytes) {
+  return guard([&] {
+    const uint64_t b = file_registry::get().release_all();
+    if (released_bytes) *released_bytes = b;
+  });
 }
 
 ts_status ts_engine_destroy(ts_engine* e) {
@@ -339,6 +349,7 @@ ts_status ts_ticket_stats_get(ts_ticket* t, ts_ticket_stats* o) {
     o->snapshot_done = s.snapshot;
     o->persisted_done = s.persisted;
     o->failed = s.failed;
+    o->file_dma_bytes = s.file_dma_bytes;
   });
 }
 

@@ -219,6 +219,10 @@ struct job {
     uint32_t fid = 0;
     uint64_t tre = header_reserved, img = 0;
     std::unique_ptr<file_writer> w;
+    // fixed region page-locked in file_registry: D2H windows land in the file
+    uint8_t* dma = nullptr;
+    file_key key;
+    bool claimed = false, released = false;
     int win_pending = 0, raw_pending = 0, struct_pending = 0;
     bool appended = true, finalizing = false, finalized = false;
     std::vector<size_t> structs;
@@ -228,6 +232,8 @@ struct job {
   struct win {
     uint64_t lo = 0, hi = 0;
     pinned_pool::region r;
+    uint8_t* host = nullptr;  // landing address: the pool region, or the file pages (dma)
+    bool dma = false;
     cudaEvent_t ev = nullptr;
     int refs = 0;
     uint32_t wp_begin = 0, wp_end = 0, fs_begin = 0, fs_end = 0, hp_begin = 0, hp_end = 0;
@@ -269,6 +275,7 @@ struct job {
   std::vector<cudaEvent_t> chunk_events;  // per-job, destroyed at the end
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pack_events;  // kernel-only pack timing
   uint64_t img = 0;
+  uint64_t win_bytes = 0;  // D2H window size W: windows are cut at multiples of W
   bool io = true;
   // device checksums (checksum_on_gpu): device-tier raw objects hashed by the
   // FNV kernels; results land in a pool region
@@ -282,6 +289,8 @@ struct job {
   cudaEvent_t fnv_ev = nullptr;
 
   ~job() {
+    for (auto& f : files)  // a claimed file that never finalized: its pages may be stale
+      if (f.claimed && !f.released) file_registry::get().release(f.key, -1, false);
     for (auto e : chunk_events)
       if (e) cudaEventDestroy(e);
     for (auto& pe : pack_events) {
@@ -464,7 +473,10 @@ std::shared_ptr<ticket_state> engine::issue(session& s, const ts_rank_info& rank
   // [img, img + tre - 4096), file images 4 KiB aligned so that every object
   // starts 16-B aligned in the image.
   const std::string rdir = s.rank_dir(rank.rank_id);
-  if (j->io) mkdirs(rdir);
+  if (j->io) {
+    mkdirs(rdir);
+    file_registry::get().sweep();  // registrations of deleted checkpoints
+  }
   std::unordered_map<uint32_t, uint32_t> fidx;
   uint64_t cursor = 0;
   for (const auto& fp : j->plan.files) {
@@ -477,10 +489,25 @@ std::shared_ptr<ticket_state> engine::issue(session& s, const ts_rank_info& rank
     const std::string fname = "file_" + std::to_string(fp.file_id) + ".bin";
     const std::string recycled =
         spare_dir_.empty() ? std::string() : spare_dir_ + "/" + rank_dir_name(rank.rank_id) + "_" + fname;
+    // Every opened file passes through the registry before it is truncated
+    // (locked pages must never be dropped); a valid registration of exactly
+    // [0, tre) makes the file's D2H windows land in its pages.
+    auto on_open = [&](int fd) {
+      uint8_t* m = file_registry::get().claim(fd, fp.tensor_region_end, &fs.key);
+      if (!m) return false;
+      fs.claimed = true;
+      if (cfg_.file_dma && fp.tensor_region_end > header_reserved) {
+        fs.dma = m;
+      } else {  // not wanted here: drop it before the file changes
+        file_registry::get().release(fs.key, -1, false);
+        fs.released = true;
+      }
+      return fs.dma != nullptr;
+    };
     fs.w = std::make_unique<file_writer>(rdir + "/" + fname, fp.tensor_region_end, j->plan.hash,
-                                         cfg_.overwrite != 0, j->io, recycled);
+                                         cfg_.overwrite != 0, j->io, recycled, on_open);
     fs.append_end = fp.tensor_region_end;
-    if (cfg_.flush_mmap) fs.w->map_fixed_region();
+    if (cfg_.flush_mmap && !fs.dma) fs.w->map_fixed_region();
     fidx.emplace(fp.file_id, static_cast<uint32_t>(j->files.size()));
     j->files.push_back(std::move(fs));
   }
@@ -526,36 +553,41 @@ std::shared_ptr<ticket_state> engine::issue(session& s, const ts_rank_info& rank
 
   // D2H windows over [0, img) and their pieces (one sweep).
   const uint64_t W = std::min<uint64_t>(cfg_.raw_chunk_bytes, pool_->capacity());
+  j->win_bytes = W;
+  // Windows lie inside one file's fixed region (so a window has one contiguous
+  // landing range: a pool region or the file's locked pages) and inside one
+  // W-aligned slice of the image (so inside one ring chunk); the 4 KiB padding
+  // between file images is never transferred.
   {
-    size_t ri = 0, fi = 0;
-    for (uint64_t lo = 0; lo < j->img; lo += W) {
-      job::win w;
-      w.lo = lo;
-      w.hi = std::min(lo + W, j->img);
-      w.wp_begin = static_cast<uint32_t>(j->wp.size());
-      w.fs_begin = static_cast<uint32_t>(j->fs.size());
-      w.hp_begin = static_cast<uint32_t>(j->hp.size());
-      while (ri < j->raws.size() && j->raws[ri].img + j->raws[ri].size <= w.lo) ++ri;
-      for (size_t k = ri; k < j->raws.size() && j->raws[k].img < w.hi; ++k) {
-        const auto& r = j->raws[k];
-        const uint64_t a = std::max(w.lo, r.img), b = std::min(w.hi, r.img + r.size);
-        if (b <= a) continue;
-        j->wp.push_back({static_cast<uint32_t>(k), b - a, a - w.lo});
-        if (!r.device) j->hp.push_back({r.src + (a - r.img), b - a, a - w.lo});
-      }
-      while (fi < j->files.size() && j->files[fi].img + (j->files[fi].tre - header_reserved) <= w.lo) ++fi;
-      for (size_t k = fi; k < j->files.size() && j->files[k].img < w.hi; ++k) {
-        auto& f = j->files[k];
-        const uint64_t fe = f.img + (f.tre - header_reserved);
-        const uint64_t a = std::max(w.lo, f.img), b = std::min(w.hi, fe);
-        if (b <= a) continue;
-        j->fs.push_back({static_cast<uint32_t>(k), header_reserved + (a - f.img), b - a, a - w.lo});
+    size_t ri = 0;
+    for (size_t fi = 0; fi < j->files.size(); ++fi) {
+      auto& f = j->files[fi];
+      const uint64_t fe = f.img + (f.tre - header_reserved);
+      for (uint64_t lo = f.img; lo < fe;) {
+        job::win w;
+        w.lo = lo;
+        w.hi = std::min(fe, (lo / W + 1) * W);
+        lo = w.hi;
+        w.dma = j->io && f.dma != nullptr;
+        w.wp_begin = static_cast<uint32_t>(j->wp.size());
+        w.fs_begin = static_cast<uint32_t>(j->fs.size());
+        w.hp_begin = static_cast<uint32_t>(j->hp.size());
+        while (ri < j->raws.size() && j->raws[ri].img + j->raws[ri].size <= w.lo) ++ri;
+        for (size_t k = ri; k < j->raws.size() && j->raws[k].img < w.hi; ++k) {
+          const auto& r = j->raws[k];
+          const uint64_t a = std::max(w.lo, r.img), b = std::min(w.hi, r.img + r.size);
+          if (b <= a) continue;
+          j->wp.push_back({static_cast<uint32_t>(k), b - a, a - w.lo});
+          if (!r.device) j->hp.push_back({r.src + (a - r.img), b - a, a - w.lo});
+        }
+        j->fs.push_back({static_cast<uint32_t>(fi), header_reserved + (w.lo - f.img), w.hi - w.lo, 0});
         if (j->io) f.win_pending += 1;
+        if (w.dma) w.host = f.dma + header_reserved + (w.lo - f.img);
+        w.wp_end = static_cast<uint32_t>(j->wp.size());
+        w.fs_end = static_cast<uint32_t>(j->fs.size());
+        w.hp_end = static_cast<uint32_t>(j->hp.size());
+        j->wins.push_back(w);
       }
-      w.wp_end = static_cast<uint32_t>(j->wp.size());
-      w.fs_end = static_cast<uint32_t>(j->fs.size());
-      w.hp_end = static_cast<uint32_t>(j->hp.size());
-      j->wins.push_back(w);
     }
     std::vector<std::pair<double, uint32_t>> key(j->wins.size());
     for (size_t k = 0; k < j->wins.size(); ++k) {
@@ -707,7 +739,12 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     j->wins_enqueued += 1;
   };
   auto acquire = [&](job::win& w) {
-    w.r = pool_->acquire(w.hi - w.lo, timeout >= 0 ? now_ns() + timeout : -1);
+    if (w.dma) {  // lands in the file's locked pages: no pool region
+      t.file_dma_bytes += w.hi - w.lo;
+    } else {
+      w.r = pool_->acquire(w.hi - w.lo, timeout >= 0 ? now_ns() + timeout : -1);
+      w.host = pool_->data(w.r);
+    }
     w.ev = get_event();
   };
   auto failed = [&] {
@@ -719,7 +756,7 @@ void engine::run_job(const std::shared_ptr<job>& j) {
   // else a ring of `nslots` chunks of whole windows (>= 1 GiB each when the
   // ring allows), packs running ahead of the copies, so the capture completes
   // once all but the last ring-full of the image has left the device.
-  const uint64_t W = j->wins.empty() ? 0 : j->wins.front().hi - j->wins.front().lo;
+  const uint64_t W = j->win_bytes;
   uint64_t chunk = 0;
   size_t nslots = 0, nchunks = 0;
   uint8_t* ring = nullptr;
@@ -915,8 +952,15 @@ void engine::run_job(const std::shared_ptr<job>& j) {
         const size_t wi = shadow ? j->worder[q] : q;
         auto& win = j->wins[wi];
         acquire(win);
-        cuda_check(cudaMemcpyAsync(pool_->data(win.r), slot + (win.lo - clo), win.hi - win.lo,
-                                   cudaMemcpyDeviceToHost, copy_stream_), "D2H window");
+        const cudaError_t ce = cudaMemcpyAsync(win.host, slot + (win.lo - clo), win.hi - win.lo,
+                                               cudaMemcpyDeviceToHost, copy_stream_);
+        if (ce != cudaSuccess) {
+          char m[256];
+          std::snprintf(m, sizeof m, "D2H window [%llu, %llu) of chunk %zu at %llu (ring %llu B, host %p dma %d)",
+                        (unsigned long long)win.lo, (unsigned long long)win.hi, c, (unsigned long long)clo,
+                        (unsigned long long)ring_bytes_, (void*)win.host, (int)win.dma);
+          cuda_check(ce, m);
+        }
         t.copies += 1;
         cuda_check(cudaEventRecord(win.ev, copy_stream_), "event");
         push_window(wi);
@@ -937,7 +981,15 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       const size_t w = j->worder[q];
       auto& win = j->wins[w];
       acquire(win);
-      dev::launch_pack(d_segs, nsegs, win.lo, win.hi, dbase + win.r.offset, ctas, threads, pack_stream_);
+      uint8_t* dst = nullptr;  // device view of the mapped pool region / locked file pages
+      if (win.dma) {
+        const auto& f = j->files[j->fs[win.fs_begin].f];
+        cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dst), f.dma, 0), "cudaHostGetDevicePointer");
+        dst += win.host - f.dma;
+      } else {
+        dst = dbase + win.r.offset;
+      }
+      dev::launch_pack(d_segs, nsegs, win.lo, win.hi, dst, ctas, threads, pack_stream_);
       t.kernel_launches += 1;
       cuda_check(cudaGetLastError(), "pack kernel launch");
       cuda_check(cudaEventRecord(win.ev, pack_stream_), "event");
@@ -951,7 +1003,7 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       const size_t w = j->worder[q];
       auto& win = j->wins[w];
       acquire(win);
-      uint8_t* dst = pool_->data(win.r);
+      uint8_t* dst = win.host;
       size_t k = std::upper_bound(j->segs.begin(), j->segs.end(), win.lo,
                                   [](uint64_t x, const dev::seg& sg) { return x < sg.pos; }) - j->segs.begin();
       k = k ? k - 1 : 0;
@@ -1010,7 +1062,7 @@ void engine::completer_loop() {
         std::lock_guard<std::mutex> g(j->mu);
         j->wins_landed += 1;
       }
-      pool_->release(win.r);
+      if (!win.dma) pool_->release(win.r);
       continue;
     }
     {
@@ -1025,14 +1077,17 @@ void engine::completer_loop() {
 void engine::window_landed(const std::shared_ptr<job>& j, size_t wi) {
   auto& w = j->wins[wi];
   TRACE("landed rank=%d w=%zu pieces=%u fsegs=%u", j->rank_id, wi, w.wp_end - w.wp_begin, w.fs_end - w.fs_begin);
-  uint8_t* base = pool_->data(w.r);
+  uint8_t* base = w.host;
   for (uint32_t k = w.hp_begin; k < w.hp_end; ++k)
     std::memcpy(base + j->hp[k].win_off, j->hp[k].src, j->hp[k].len);  // host-tier bytes
   size_t newly_ready = 0;
   bool release_now = false;
   {
     std::lock_guard<std::mutex> g(j->mu);
-    w.refs = (j->io && w.fs_end > w.fs_begin) ? 1 : 0;
+    // a pool window holds one reference for its flush; a dma window is already in the file
+    w.refs = (j->io && !w.dma && w.fs_end > w.fs_begin) ? 1 : 0;
+    if (j->io && w.dma)
+      for (uint32_t k = w.fs_begin; k < w.fs_end; ++k) j->files[j->fs[k].f].win_pending -= 1;
     for (uint32_t k = w.wp_begin; k < w.wp_end; ++k) {
       auto& r = j->raws[j->wp[k].obj];
       if (j->gpu_ck && r.device) continue;  // checksummed on the device
@@ -1047,7 +1102,7 @@ void engine::window_landed(const std::shared_ptr<job>& j, size_t wi) {
     j->wins_landed += 1;
     release_now = w.refs == 0;
   }
-  if (release_now) pool_->release(w.r);
+  if (release_now && !w.dma) pool_->release(w.r);
   bool last;
   {
     std::lock_guard<std::mutex> g(j->mu);
@@ -1055,9 +1110,12 @@ void engine::window_landed(const std::shared_ptr<job>& j, size_t wi) {
   }
   if (last)
     for (size_t f = 0; f < j->files.size(); ++f) file_progress(j, f);
+  else if (j->io && w.dma)
+    for (uint32_t k = w.fs_begin; k < w.fs_end; ++k) file_progress(j, j->fs[k].f);
   for (size_t k = 0; k < (newly_ready + 3) / 4; ++k)
     workers_->submit(guarded(j, [this, j] { hash_task(j, 0); }));
-  if (j->io && w.fs_end > w.fs_begin) workers_->submit(guarded(j, [this, j, wi] { flush_window(j, wi); }));
+  if (j->io && !w.dma && w.fs_end > w.fs_begin)
+    workers_->submit(guarded(j, [this, j, wi] { flush_window(j, wi); }));
   check_snapshot(j);
 }
 
@@ -1086,7 +1144,7 @@ void engine::window_release_ref(const std::shared_ptr<job>& j, size_t wi) {
     std::lock_guard<std::mutex> g(j->mu);
     rel = --j->wins[wi].refs == 0;
   }
-  if (rel) pool_->release(j->wins[wi].r);
+  if (rel && !j->wins[wi].dma) pool_->release(j->wins[wi].r);
 }
 
 namespace {
@@ -1214,7 +1272,7 @@ void engine::hash_task(const std::shared_ptr<job>& j, size_t) {
 
 void engine::flush_window(const std::shared_ptr<job>& j, size_t wi) {
   auto& w = j->wins[wi];
-  const uint8_t* base = pool_->data(w.r);
+  const uint8_t* base = w.host;
   bool ok = true;
   {
     std::lock_guard<std::mutex> g(j->t->mu);
@@ -1360,6 +1418,21 @@ void engine::file_progress(const std::shared_ptr<job>& j, size_t fi) {
   } catch (const error& e) {
     j->t->fail(e.status, std::string("finalize failed: ") + e.what(), e.object_id);
     return;
+  }
+  if (j->io && f.w->fd() >= 0) {
+    // Locked-page bookkeeping: stamp a used registration; with rotation on,
+    // lock a new file's pages in the background for when it is recycled.
+    auto& reg = file_registry::get();
+    if (f.claimed && !f.released) {
+      reg.release(f.key, f.w->fd(), true);
+      f.released = true;
+    } else if (cfg_.file_dma && !spare_dir_.empty() && f.tre > header_reserved) {
+      file_key k;
+      if (reg.want_register(f.w->fd(), f.tre, &k)) {
+        const int dev = device_;
+        workers_->submit([k, dev] { file_registry::get().register_file(k, dev); });
+      }
+    }
   }
   bool all = false;
   {

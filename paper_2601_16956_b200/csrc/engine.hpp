@@ -27,6 +27,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "filereg.hpp"
 #include "format.hpp"
 #include "kernels.cuh"
 
@@ -92,6 +93,7 @@ struct ticket_state {
   int64_t t_issue = 0, t_captured = -1, t_snapshot = -1, t_persisted = -1;
   int64_t issue_block_ns = 0, barrier_block_ns = 0;
   uint64_t total_bytes = 0, raw_bytes = 0, serialized_bytes = 0, image_bytes = 0;
+  uint64_t file_dma_bytes = 0;  // fixed-region bytes DMA'd straight into file pages
   float pack_ms = 0, d2h_ms = 0;
   uint32_t kernel_launches = 0, copies = 0;
   cudaEvent_t ev_start = nullptr, ev_capture = nullptr, ev_d2h_first = nullptr,

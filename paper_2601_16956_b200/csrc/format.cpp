@@ -159,7 +159,7 @@ void pread_all(int fd, void* p, size_t n, uint64_t off, const std::string& path)
 
 // format.cpp:125-147: header block, pre-size to tensor_region_end.
 file_writer::file_writer(const std::string& path, uint64_t tre, uint64_t plan_hash, bool overwrite,
-                         bool io, const std::string& recycled)
+                         bool io, const std::string& recycled, const std::function<bool(int)>& on_open)
     : path_(path), tre_(tre), io_(io) {
   if (!io_) return;
   if (!overwrite && ::access(path.c_str(), F_OK) == 0) fail(TS_ERR_IO, "file exists: " + path);
@@ -167,8 +167,16 @@ file_writer::file_writer(const std::string& path, uint64_t tre, uint64_t plan_ha
     fd_ = ::open(path.c_str(), O_RDWR);
     reused_ = fd_ >= 0;
   }
-  if (fd_ < 0) fd_ = ::open(path.c_str(), O_RDWR | O_CREAT | O_TRUNC, 0644);
+  bool fresh = false;
+  if (fd_ < 0) {
+    fd_ = ::open(path.c_str(), O_RDWR | O_CREAT, 0644);
+    fresh = true;
+  }
   if (fd_ < 0) fail(TS_ERR_IO, "cannot create " + path + ": " + std::strerror(errno));
+  const bool keep = on_open ? on_open(fd_) : false;
+  // (O_TRUNC semantics for a new file, after on_open had its look at the inode)
+  if (fresh && !keep && ::ftruncate(fd_, 0) != 0)
+    fail(TS_ERR_IO, "cannot truncate " + path + ": " + std::strerror(errno));
   uint8_t header[header_reserved] = {};
   std::memcpy(header, "TSCKPT01", 8);
   put_u32(header + 8, 1);

@@ -8,6 +8,7 @@
 //   MANIFEST.tlv                   format.cpp:292-405
 #pragma once
 
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -55,8 +56,13 @@ class file_writer {
   // creating a fresh one: its page-cache pages are reused, every byte the
   // checkpoint needs is rewritten (header, whole fixed region incl. zero gaps,
   // appends, footer; the old tail is truncated away).
+  // `on_open(fd)` runs right after open, before the header is written or the
+  // file is truncated; it returns true when the file's existing pages in
+  // [0, tensor_region_end) must be kept (a page-locked registration of them is
+  // in use, filereg.hpp): the file is then only re-sized, never emptied first.
   file_writer(const std::string& path, uint64_t tensor_region_end, uint64_t plan_hash,
-              bool overwrite, bool io, const std::string& recycled = "");
+              bool overwrite, bool io, const std::string& recycled = "",
+              const std::function<bool(int)>& on_open = {});
   ~file_writer();
   void write_at(uint64_t off, const void* p, size_t n);
   // Fixed-region writes through a shared mapping of [0, tensor_region_end):
@@ -74,6 +80,7 @@ class file_writer {
   // is not free: done after the file is reported persisted).
   void release_mapping();
   const std::string& path() const { return path_; }
+  int fd() const { return fd_; }
 
  private:
   std::string path_;

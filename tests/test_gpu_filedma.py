@@ -1,0 +1,187 @@
+"""Direct D2H into page-locked checkpoint files (file_dma, csrc/filereg.hpp).
+
+With checkpoint rotation, a finalized file's fixed region is page-locked in the
+background; when the file is recycled for a later checkpoint of the same
+layout, the copy engines write the D2H windows straight into its page-cache
+pages. Every case must stay byte-identical to the reference's trees, and a
+registration must never be used for a file that changed behind our back."""
+import os
+import shutil
+import tempfile
+
+import pytest
+
+from conftest import GOLDEN, read_tree
+from gpu_helpers import checkpoint_recipe
+from paper_2601_16956_b200 import api
+from paper_2601_16956_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def shm():
+    if not os.path.isdir("/dev/shm"):
+        pytest.skip("needs tmpfs /dev/shm")
+    d = tempfile.mkdtemp(dir="/dev/shm", prefix="ts_filedma_")
+    yield d
+    shutil.rmtree(d, ignore_errors=True)
+    api.file_cache_release_all()
+
+
+def cfg_for(mode, **kw):
+    extra = {}
+    if mode == "ring-bulk":
+        mode, extra = "ring", dict(pack_kernel="bulk", bulk_min_bytes=32768)
+    base = dict(d2h_mode=mode, raw_chunk_bytes=64 << 10, staging_capacity_bytes=1 << 20,
+                device_staging_bytes=256 << 10, flush_workers=3, **extra)
+    base.update(kw)
+    return api.EngineConfig(**base)
+
+
+def fixed_bytes(rec, tso):
+    """Σ fixed-region bytes [4096, tensor_region_end) over every rank file
+    (plan from the oracle's restatement: test-side checker only)."""
+    tot = 0
+    for r in rec.ranks:
+        objs = [tso.Obj(o.object_id, o.kind, o.tier, o.precision, o.file_id, o.size) for o in r.objects]
+        tot += sum(fp.tensor_region_end - 4096 for fp in tso.plan_layout(objs).values())
+    return tot
+
+
+def rotate(rec, shm, cfg, rounds=3, tamper=None):
+    """`rounds` checkpoints of the same state, each new one recycling the files
+    of the one before (retired into a spare directory); engines are recreated
+    per checkpoint, so their shutdown waits for the background page locking."""
+    spare = os.path.join(shm, "spare")
+    stats = []
+    prev = None
+    for k in range(rounds):
+        if prev:
+            api.retire_checkpoint(prev, spare)
+            if tamper:
+                tamper(spare)
+        out = os.path.join(shm, f"c{k}")
+        session = api.CheckpointSession(out, rec.ckpt_id, rec.iteration, rec.manifest_echo(),
+                                        n_ranks=len(rec.ranks))
+        states = [api.materialize_payloads(r, 0, rec.pit) for r in rec.ranks]
+        engines = [api.CheckpointEngine(cfg, r.rank_id, 0) for r in rec.ranks]
+        for e in engines:
+            e.set_spare_dir(spare)
+        tickets = [e.issue_checkpoint(session, s, rec.iteration) for e, s in zip(engines, states)]
+        for t in tickets:
+            t.wait_persisted()
+        session.wait_complete(120)
+        stats.append([t.stats() for t in tickets])
+        for e in engines:
+            e.shutdown()
+        assert read_tree(out) == read_tree(os.path.join(GOLDEN, "trees", rec_name(rec))), f"checkpoint {k}"
+        prev = out
+    return stats
+
+
+def rec_name(rec):
+    return rec._golden_name
+
+
+def load(name):
+    rec = S.load_recipe(os.path.join(GOLDEN, "recipes", name + ".recipe"))
+    rec._golden_name = name
+    return rec
+
+
+@pytest.mark.parametrize("mode", ["ring", "direct", "zerocopy", "ring-bulk"])
+@pytest.mark.parametrize("name", ["hand_mixed", "odd_layout", "zero3_tiny", "two_ranks"])
+def test_recycled_files_take_direct_dma(gpu, shm, oracle, name, mode):
+    rec = load(name)
+    stats = rotate(rec, shm, cfg_for(mode))
+    dma0 = sum(s["file_dma_bytes"] for s in stats[0])
+    dma1 = sum(s["file_dma_bytes"] for s in stats[1])
+    dma2 = sum(s["file_dma_bytes"] for s in stats[2])
+    assert dma0 == 0  # fresh files: pool + flush
+    assert dma1 == dma2 == fixed_bytes(rec, oracle) > 0  # every fixed-region byte straight into the file
+
+
+@pytest.mark.parametrize("mode", ["ring", "direct"])
+def test_direct_dma_host_checksums(gpu, shm, oracle, mode):
+    """checksum_on_gpu=0: host FNV workers hash the pieces in the file pages."""
+    rec = load("hand_mixed")
+    stats = rotate(rec, shm, cfg_for(mode, checksum_on_gpu=False))
+    assert sum(s["file_dma_bytes"] for s in stats[1]) == fixed_bytes(rec, oracle)
+
+
+def test_file_dma_off_uses_pool(gpu, shm):
+    rec = load("odd_layout")
+    stats = rotate(rec, shm, cfg_for("ring", file_dma=False))
+    assert all(s["file_dma_bytes"] == 0 for ss in stats for s in ss)
+    assert api.file_cache_bytes() == 0
+
+
+def test_tampered_file_is_not_trusted(gpu, shm):
+    """A recycled file truncated behind the registry's back (size/mtime stamp
+    changed) is not written through its stale locked pages."""
+    rec = load("odd_layout")
+
+    def tamper(spare):
+        for f in sorted(os.listdir(spare)):
+            p = os.path.join(spare, f)
+            sz = os.path.getsize(p)
+            if sz > 8192:
+                os.truncate(p, 4096)
+                os.truncate(p, sz)
+                with open(p, "r+b") as fh:
+                    fh.seek(5000)
+                    fh.write(b"x")
+
+    stats = rotate(rec, shm, cfg_for("ring"), rounds=2, tamper=tamper)
+    assert sum(s["file_dma_bytes"] for s in stats[1]) == 0
+
+
+def test_layout_change_drops_registration(gpu, shm):
+    """Files recycled for a different layout (other tensor_region_end) fall back
+    to the pool path, and the bytes stay identical."""
+    a, b = load("tiny_layout"), load("two_ranks")
+    for r, o in zip(b.ranks, a.ranks):
+        o.rank_id = r.rank_id
+    a.ranks = a.ranks[:len(b.ranks)]
+    spare = os.path.join(shm, "spare")
+    cfg = cfg_for("ring")
+    old = os.path.join(shm, "old")
+    sess = api.CheckpointSession(old, a.ckpt_id, a.iteration, a.manifest_echo(), n_ranks=len(a.ranks))
+    engines = [api.CheckpointEngine(cfg, r.rank_id, 0) for r in a.ranks]
+    for e in engines:
+        e.set_spare_dir(spare)
+    states = [api.materialize_payloads(r, 0, a.pit) for r in a.ranks]
+    for t in [e.issue_checkpoint(sess, s, a.iteration) for e, s in zip(engines, states)]:
+        t.wait_persisted()
+    sess.wait_complete(60)
+    for e in engines:
+        e.shutdown()
+    assert api.file_cache_bytes() > 0
+    api.retire_checkpoint(old, spare)
+    new = os.path.join(shm, "new")
+    sess = api.CheckpointSession(new, b.ckpt_id, b.iteration, b.manifest_echo(), n_ranks=len(b.ranks))
+    engines = [api.CheckpointEngine(cfg, r.rank_id, 0) for r in b.ranks]
+    for e in engines:
+        e.set_spare_dir(spare)
+    states = [api.materialize_payloads(r, 0, b.pit) for r in b.ranks]
+    tickets = [e.issue_checkpoint(sess, s, b.iteration) for e, s in zip(engines, states)]
+    for t in tickets:
+        t.wait_persisted()
+    sess.wait_complete(60)
+    assert all(t.stats()["file_dma_bytes"] == 0 for t in tickets)
+    for e in engines:
+        e.shutdown()
+    assert read_tree(new) == read_tree(os.path.join(GOLDEN, "trees", "two_ranks"))
+
+
+def test_deleted_files_are_unlocked(gpu, shm):
+    rec = load("hand_mixed")
+    rotate(rec, shm, cfg_for("ring"), rounds=2)
+    assert api.file_cache_bytes() > 0
+    for d in os.listdir(shm):
+        shutil.rmtree(os.path.join(shm, d))
+    # the next issue sweeps registrations of unlinked files
+    out = os.path.join(shm, "after")
+    checkpoint_recipe(rec, out, cfg_for("ring"))
+    assert api.file_cache_bytes() == 0
