@@ -81,6 +81,30 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def ncu_traffic(cfg: str, mode: str, pack_kernel: str):
+    """DRAM bytes per pack launch from the committed ncu --set full capture of
+    this workload (profiles/ncu_traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+    except Exception:
+        return None
+    if t.get("workload") != cfg or mode != "ring" or pack_kernel != "warp":
+        return None
+    return int(t["traffic_bytes_per_launch"])
+
+
+def host_mem_avail() -> int:
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except Exception:
+        pass
+    return 0
+
+
 def dist_info():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -190,27 +214,45 @@ def ours(args):
     from paper_2601_16956_b200 import synthetic as S
 
     ws, rank, local = dist_info()
+    # One GPU per rank (NCCL). TS_BENCH_SHARE_GPU=1 runs the N>1 path on fewer
+    # GPUs than ranks (gloo, ranks share devices) — a functional check of the
+    # multi-rank code path on a 1-GPU box, never a scaling number.
+    share = os.environ.get("TS_BENCH_SHARE_GPU") == "1"
+    local_dev = local % torch.cuda.device_count() if share else local
+    backend = "gloo" if share else "nccl"
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
+    cdev = torch.device("cpu") if backend == "gloo" else dev  # collective tensors
 
     rec = S.config_recipe(args.config, rank)
     spec = rec.ranks[0]
-    state = api.materialize_payloads(spec, local, 0)
+    state = api.materialize_payloads(spec, local_dev, 0)
     raw = spec.raw_bytes
     img_est = raw + 4096 * (len(spec.objects) + 4)
-    free, _ = torch.cuda.mem_get_info(local)
+    free, _ = torch.cuda.mem_get_info(local_dev)
     shadow = img_est + (256 << 20) <= free - (24 << 30)  # keep room for the GEMM load
+    # no full shadow: the largest ring that leaves the same room (--ring-gb overrides)
+    ring_bytes = int(args.ring_gb * (1 << 30)) if args.ring_gb else max(8 << 30, free - (26 << 30))
     # pinned pool: the whole image when host RAM allows (one pinning at engine
     # creation), else a bounded pool with back-pressure (staging.cpp semantics)
+    local_ws = int(os.environ.get("LOCAL_WORLD_SIZE", str(ws)))
+    avail = host_mem_avail()
     pool_cap = int(args.pool_gb * (1 << 30)) if args.pool_gb else 64 << 30
+    if avail:  # every rank of this node pins its pool: stay well inside host RAM
+        pool_cap = min(pool_cap, max(1 << 30, int(0.3 * avail / max(1, local_ws))))
     pool = (min(img_est + (64 << 20), pool_cap) + (2 << 20) - 1) // (2 << 20) * (2 << 20)
     cfg = api.EngineConfig(d2h_mode=args.mode, staging_capacity_bytes=pool, raw_chunk_bytes=64 << 20,
-                           device_staging_bytes=img_est + (1 << 20) if shadow else int(args.ring_gb * (1 << 30)),
+                           device_staging_bytes=img_est + (1 << 20) if shadow else ring_bytes,
                            flush_workers=args.flush_workers or min(16, os.cpu_count() or 8), write_files=False,
-                           checksum_on_gpu=not args.host_checksum, pack_kernel=args.pack_kernel)
-    eng = api.CheckpointEngine(cfg, spec.rank_id, local)
+                           checksum_on_gpu=not args.host_checksum, pack_kernel=args.pack_kernel,
+                           checksum_priority=args.ck_priority, pack_priority=args.pack_priority,
+                           checksum_host_frac=args.ck_host_frac, ring_chunk_bytes=int(args.ring_chunk_gb * (1 << 30)))
+    eng = api.CheckpointEngine(cfg, spec.rank_id, local_dev)
     full = getattr(rec, "full_layout", None)
     echo = S.Recipe(layout=full).manifest_echo() if full else rec.manifest_echo()
     tdir = os.path.join("/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir(), "ts_bench")
@@ -246,7 +288,7 @@ def ours(args):
     torch.cuda.synchronize()
     stats = []
     l0 = api.N.lib.ts_kernel_launch_count()
-    with Clocks(local) as clk:
+    with Clocks(local_dev) as clk:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
@@ -258,11 +300,11 @@ def ours(args):
     launches = api.N.lib.ts_kernel_launch_count() - l0
     t_ms = e0.elapsed_time(e1)
     if ws > 1:
-        tt = torch.tensor([t_ms], device=dev)
+        tt = torch.tensor([t_ms], device=cdev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
     bytes_step = stats[0]["total_bytes"]
-    tot = torch.tensor([float(bytes_step)], device=dev)
+    tot = torch.tensor([float(bytes_step)], device=cdev)
     if ws > 1:
         dist.all_reduce(tot)
     box_bytes = float(tot.item())
@@ -278,20 +320,38 @@ def ours(args):
     # --- e2e through the public API with files on /dev/shm -------------------
     e2e = None
     if args.e2e_steps > 0:
+        # files kept on tmpfs: the retention window + the checkpoint in flight, per rank of the node
+        try:
+            st_shm = os.statvfs(os.path.dirname(tdir))
+            shm_free = st_shm.f_bavail * st_shm.f_frsize
+        except OSError:
+            shm_free = 0
+        # (rotation recycles the retired files: at most `keep` checkpoints exist at once)
+        need = max(1, args.keep) * img_est * local_ws
+        fits = not (shm_free and need > 0.85 * shm_free)
+        if ws > 1:  # the same decision on every rank (the e2e phase has collectives)
+            ft = torch.tensor([1 if fits else 0], device=cdev)
+            dist.all_reduce(ft, op=dist.ReduceOp.MIN)
+            fits = bool(ft.item())
+        if not fits:
+            print(f"bench: e2e skipped, needs ~{need / 1e9:.0f} GB of {shm_free / 1e9:.0f} GB tmpfs per node "
+                  f"(use --keep 1)", file=sys.stderr)
+            args.e2e_steps = 0
+    if args.e2e_steps > 0:
         cfg_io = api.EngineConfig(**{**cfg.__dict__, "write_files": True})
         eng.shutdown()
-        eng_io = api.CheckpointEngine(cfg_io, spec.rank_id, local)
+        eng_io = api.CheckpointEngine(cfg_io, spec.rank_id, local_dev)
         spare = os.path.join(tdir, ".spare")
         if not args.fresh_files:
             eng_io.set_spare_dir(spare)
         # warm the file path: with rotation, 2 checkpoints fill the retention
         # window (fresh files, pool + flush; their pages get locked in the
         # background) and 2 more recycle them — the steady state is reached
-        nwarm = 2 if args.fresh_files else 4
+        nwarm = 2 if args.fresh_files else 2 * args.keep
         for w in range(nwarm):
             it += 1
-            old = os.path.join(tdir, f"ckpt_{it - 2:06d}")
-            if not args.fresh_files and w >= 2 and rank == 0 and os.path.exists(old):
+            old = os.path.join(tdir, f"ckpt_{it - args.keep:06d}")
+            if not args.fresh_files and w >= args.keep and rank == 0 and os.path.exists(old):
                 api.retire_checkpoint(old, spare)
             if ws > 1:
                 dist.barrier()
@@ -304,8 +364,8 @@ def ours(args):
         dma = []
         for _ in range(args.e2e_steps):
             it += 1
-            # rotation: keep the last 2 checkpoints, recycle older files
-            old = os.path.join(tdir, f"ckpt_{it - 2:06d}")
+            # rotation: keep the last `keep` checkpoints, recycle older files
+            old = os.path.join(tdir, f"ckpt_{it - args.keep:06d}")
             if not args.fresh_files and rank == 0 and os.path.exists(old):
                 api.retire_checkpoint(old, spare)
             if ws > 1:
@@ -316,7 +376,7 @@ def ours(args):
         torch.cuda.synchronize()
         e2e_ms = f0.elapsed_time(f1)
         if ws > 1:
-            tt = torch.tensor([e2e_ms], device=dev)
+            tt = torch.tensor([e2e_ms], device=cdev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e2e_ms = float(tt.item())
         e2e = {"value": round(box_bytes * args.e2e_steps / (e2e_ms / 1e3) / 1e9, 3), "unit": "GB/s",
@@ -325,17 +385,25 @@ def ours(args):
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(image),
                "file_dma_frac": round(sum(dma) / (len(dma) * image), 3) if dma else 0.0,
                "what": "issue -> files + footers + MANIFEST.tlv durable on /dev/shm, via the C-ABI"
-                       + ("" if args.fresh_files else "; rotation keeps 2 checkpoints, older files recycled, "
+                       + ("" if args.fresh_files else f"; rotation keeps {args.keep} checkpoint(s), older files recycled, "
                           "D2H windows land directly in their page-locked pages (file_dma)")}
         # restore of the last checkpoint (H2D + scatter-unpack + FNV verify)
         man = os.path.join(tdir, f"ckpt_{it:06d}", "MANIFEST.tlv")
         r = api.Restorer(man)
         ridx = [r.rank_info(i).rank_id for i in range(r.n_ranks)].index(spec.rank_id)
-        rs = r.restore_rank(ridx, local)
+        free_now, _ = torch.cuda.mem_get_info(local_dev)
+        if free_now > raw + (8 << 30):
+            rs = r.restore_rank(ridx, local_dev)  # fresh shards (warms the file path)
+            in_place = False
+        else:  # no room for a second copy of the shard (cfg4): restore into the state itself
+            rs, in_place = state, True
+        for o in rs.objects:  # zeroed destinations: a restore that skips bytes cannot pass
+            if o.is_raw() and o.payload is not None:
+                o.payload.zero_()
         torch.cuda.synchronize()
         t0 = time.time()
         r2 = api.Restorer(man)
-        r2.restore_rank(ridx, local, into=rs)
+        r2.restore_rank(ridx, local_dev, into=rs)
         torch.cuda.synchronize()
         restore_s = time.time() - t0
         for o, so in zip(rs.objects, spec.objects):
@@ -344,6 +412,7 @@ def ours(args):
         bad = api.pattern_mismatches(rs, it)
         e2e["restore_gbps"] = round(raw / restore_s / 1e9, 3)
         e2e["restore_bit_exact"] = bad == 0
+        e2e["restore_into"] = "the live state (zeroed first)" if in_place else "fresh, zeroed shards"
         e2e["restore_stats"] = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in r2.last_stats.items()}
         del rs, r, r2
         eng_io.shutdown()
@@ -360,7 +429,7 @@ def ours(args):
     # --- training-blocked time with a synthetic fwd/bwd load ------------------
     blocked = None
     if args.train_steps > 0:
-        blocked = training_phase(args, api, state, spec, cfg, local, dev, it)
+        blocked = training_phase(args, api, state, spec, cfg, local_dev, dev, it)
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -377,8 +446,11 @@ def ours(args):
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": f"{args.config}: {rec.name} rank-r shard, {len(spec.objects)} objects, "
                                    f"{bytes_step / 1e9:.3f} GB/rank", "d2h_mode": args.mode,
-                       "device_shadow": bool(shadow), "pinned_pool_gb": round(pool / 2**30, 2),
-                       "checksums": "host" if args.host_checksum else "gpu", "pack_kernel": args.pack_kernel, "l2": "inputs > L2 (126 MB)",
+                       "device_shadow": bool(shadow), "ring_gb": None if shadow else round(ring_bytes / 2**30, 1), "pinned_pool_gb": round(pool / 2**30, 2),
+                       "checksums": "host" if args.host_checksum else "gpu", "pack_kernel": args.pack_kernel,
+                       "priorities": {"pack": args.pack_priority, "checksums": args.ck_priority},
+                       "checksum_host_frac": "auto" if args.ck_host_frac < 0 else args.ck_host_frac,
+                       "l2": "inputs > L2 (126 MB)",
                        "step": "update(pattern kernel) + issue + snapshot + checksums (no files)"},
             "per_gpu_gbps": round(value / ws, 3),
             "snapshot_ms_mean": round(statistics.mean(snap_ms), 2),
@@ -390,7 +462,9 @@ def ours(args):
                          "bound": "hbm", "achieved": round(pack_alg / (pack_mean / 1e3) / 1e9, 1),
                          "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(pack_alg / (pack_mean / 1e3) / 1e9 / hbm_peak, 3),
-                         "traffic": None, "alg_bytes_per_launch": int(pack_alg),
+                         "traffic": ncu_traffic(args.config, args.mode, args.pack_kernel),
+                         "traffic_source": "profiles/ncu_traffic.json (ncu --set full, same workload)",
+                         "alg_bytes_per_launch": int(pack_alg),
                          "launch_ms": round(pack_mean, 3)},
             "gpu_launches": int(launches),
             "e2e": e2e, "blocked": blocked, "cpu_baseline": cpu, "clocks": clocks,
@@ -407,10 +481,50 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
     import torch
 
     run, fb_ms = gemm_load(args.fwd_bwd_ms, dev)
+    # Checkpoints go where a deployment puts them: files on tmpfs with rotation
+    # (keep `--keep`, file_dma), when tmpfs has room; else snapshot-only.
+    ws, rank, _ = dist_info()
+    local_ws = int(os.environ.get("LOCAL_WORLD_SIZE", str(ws)))
+    tdir = os.path.join("/dev/shm", f"ts_train_r{rank}")
+    files = False
+    if args.train_files and os.path.isdir("/dev/shm"):
+        st = os.statvfs("/dev/shm")
+        files = max(1, args.keep) * spec.raw_bytes * 1.01 * local_ws < 0.85 * st.f_bavail * st.f_frsize
+    if files:
+        shutil.rmtree(tdir, ignore_errors=True)
+        os.makedirs(tdir)
+        cfg = api.EngineConfig(**{**cfg.__dict__, "write_files": True})
     eng = api.CheckpointEngine(cfg, spec.rank_id, local)
+    spare = os.path.join(tdir, ".spare")
+    if files:
+        eng.set_spare_dir(spare)
+    ckpts = []  # (dir, session, ticket) on disk, oldest first
     comp = torch.cuda.current_stream()
     res = {"off": ([], []), "lazy": ([], [])}
+    host_ck = []
     it = it0
+
+    def rotate_and_issue(it):
+        while len(ckpts) >= max(1, args.keep):  # rotation (a deployment does this off-thread)
+            d0, _, t0k = ckpts.pop(0)
+            t0k.wait_persisted()
+            api.retire_checkpoint(d0, spare)
+        d = os.path.join(tdir, f"ckpt_{it:06d}")
+        sess = api.CheckpointSession(d, it, it, None, 1, writes_manifest=True)
+        return d, sess
+
+    if files:  # steady state first: the rotation window filled, recycled files page-locked
+        for _ in range(2 * max(1, args.keep)):
+            it += 1
+            api.mutate_update_step(state, it, stream=comp)
+            d, sess = rotate_and_issue(it)
+            tk = eng.issue_checkpoint(sess, state, it, producer_stream=comp)
+            ckpts.append((d, sess, tk))
+            tk.wait_persisted()
+        want = sum(max(0, (o.size + 4095) // 4096 * 4096) for o in spec.objects if o.kind == 0) * 0.9
+        t_end = time.time() + 120
+        while api.file_cache_bytes() < want * min(max(1, args.keep), len(ckpts)) and time.time() < t_end:
+            time.sleep(0.2)
     # off/lazy blocks alternate (twice) so clock / power-cap drift hits both arms
     for mode in ("off", "lazy", "off", "lazy"):
         pending = None
@@ -425,10 +539,17 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
             api.mutate_update_step(state, it, stream=comp)  # optimizer update
             ib = 0
             if mode == "lazy" and k % args.ckpt_interval == 0:
-                sess = api.CheckpointSession("", it, it, None, 1, writes_manifest=False)
+                if files:
+                    d, sess = rotate_and_issue(it)
+                else:
+                    sess = api.CheckpointSession("", it, it, None, 1, writes_manifest=False)
                 tt = time.perf_counter()
                 pending = eng.issue_checkpoint(sess, state, it, producer_stream=comp)
                 ib = time.perf_counter() - tt
+                if files:
+                    ckpts.append((d, sess, pending))
+                if k > 0:
+                    host_ck.append(pending.stats()["host_checksum_bytes"] / max(1, spec.raw_bytes))
             comp.synchronize()
             if k > 0:
                 times.append(time.perf_counter() - t0)
@@ -440,11 +561,19 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
             pending.wait_persisted()
     res = {m: (statistics.mean(t), statistics.mean(b) if b else 0.0) for m, (t, b) in res.items()}
     eng.shutdown()
+    dma = [t.stats()["file_dma_bytes"] for _, _, t in ckpts]
+    ckpts.clear()
+    if files:
+        shutil.rmtree(tdir, ignore_errors=True)
+        api.file_cache_release_all()
     off, lazy = res["off"][0], res["lazy"][0]
     return {"fwd_bwd_ms": round(fb_ms, 1), "steps": 2 * args.train_steps, "ckpt_interval": args.ckpt_interval,
             "step_ms_no_ckpt": round(1e3 * off, 2), "step_ms_lazy_ckpt": round(1e3 * lazy, 2),
             "slowdown_pct": round(100 * (lazy - off) / off, 2),
-            "blocked_ms_per_ckpt": round(res["lazy"][1], 3)}
+            "blocked_ms_per_ckpt": round(res["lazy"][1], 3),
+            "host_checksum_frac": round(statistics.mean(host_ck), 3) if host_ck else None,
+            "checkpoints_to": (f"files on /dev/shm, rotation keeps {args.keep}, file_dma bytes of the last "
+                               f"{len(dma)}: {dma}") if files else "snapshot only (pinned pool)"}
 
 
 def main():
@@ -461,12 +590,21 @@ def main():
     ap.add_argument("--ckpt-interval", type=int, default=1, help="checkpoint every k training steps")
     ap.add_argument("--host-checksum", action="store_true", help="FNV on host threads instead of the GPU kernels")
     ap.add_argument("--pack-kernel", default="warp", choices=["warp", "bulk"])
+    ap.add_argument("--ck-priority", type=int, default=-1, help="device checksum stream priority (1/0/-1)")
+    ap.add_argument("--ck-host-frac", type=float, default=-1.0,
+                    help="share of checksums on host workers (0: all GPU; <0: auto from host rate and cadence)")
+    ap.add_argument("--pack-priority", type=int, default=1, help="capture (pack) stream priority (1/0/-1)")
     ap.add_argument("--flush-workers", type=int, default=0, help="host worker threads (default: min(16, cores))")
+    ap.add_argument("--keep", type=int, default=2, help="e2e rotation: checkpoints kept on tmpfs")
+    ap.add_argument("--no-train-files", dest="train_files", action="store_false",
+                    help="training phase: snapshot only (no files)")
     ap.add_argument("--fresh-files", action="store_true",
                     help="e2e: new files every checkpoint (no rotation / recycling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pool-gb", type=float, default=0.0, help="pinned pool cap (default: image, at most 64 GiB)")
-    ap.add_argument("--ring-gb", type=float, default=8.0, help="HBM staging ring when no full device shadow fits")
+    ap.add_argument("--ring-gb", type=float, default=0.0,
+                    help="HBM staging ring when no full device shadow fits (0 = auto: free HBM - 26 GiB)")
+    ap.add_argument("--ring-chunk-gb", type=float, default=0.0, help="ring slot size (0 = auto)")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)

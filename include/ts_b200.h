@@ -182,7 +182,17 @@ typedef struct ts_engine_config {
                                        when a registration of the file exists; with a spare
                                        directory set, finalized files are registered in the
                                        background for reuse by rotation. 0: always pool + flush */
-  int32_t _pad1;
+  int32_t checksum_priority;        /* RING device checksums (they read the staged copy, off the
+                                       capture path) on their own stream: 1 highest, 0 default,
+                                       -1 lowest (default: yield the SMs to training kernels) */
+  int32_t _pad2;
+  double checksum_host_frac;        /* checksum_on_gpu=1: share of device-tier bytes hashed by host
+                                       workers instead of the FNV kernels. 0: all on the GPU;
+                                       < 0 (default): auto — sized from the measured host hashing
+                                       rate and the checkpoint cadence, objects a host chain can
+                                       finish within that time only */
+  uint64_t ring_chunk_bytes;        /* RING without a full shadow: bytes per ring slot (0 = auto:
+                                       ring/6, at most 8 GiB; rounded to whole windows) */
 } ts_engine_config;
 
 void ts_engine_config_default(ts_engine_config* cfg);
@@ -261,6 +271,7 @@ typedef struct ts_ticket_stats {
   uint32_t kernel_launches, copies;
   int32_t snapshot_done, persisted_done, failed;
   uint64_t file_dma_bytes; /* fixed-region bytes the copy engines wrote straight into file pages */
+  uint64_t host_checksum_bytes; /* device-tier bytes hashed by host workers (rest: FNV kernels) */
 } ts_ticket_stats;
 ts_status ts_ticket_stats_get(ts_ticket* t, ts_ticket_stats* out);
 /* Per-object checksum accumulated at staging (transfer.cpp:163-166) */

@@ -101,7 +101,8 @@ class EngineConfigC(C.Structure):
                 ("hybrid_direct_min_bytes", C.c_uint64), ("pack_ctas", C.c_int32),
                 ("pack_threads", C.c_int32), ("pack_priority", C.c_int32), ("write_files", C.c_int32),
                 ("checksum_on_gpu", C.c_int32), ("flush_mmap", C.c_int32), ("pack_kernel", C.c_int32),
-                ("bulk_min_bytes", C.c_uint64), ("file_dma", C.c_int32), ("_pad1", C.c_int32)]
+                ("bulk_min_bytes", C.c_uint64), ("file_dma", C.c_int32), ("checksum_priority", C.c_int32),
+                ("_pad2", C.c_int32), ("checksum_host_frac", C.c_double), ("ring_chunk_bytes", C.c_uint64)]
 
 
 class ManifestEcho(C.Structure):
@@ -117,7 +118,8 @@ class TicketStats(C.Structure):
                 ("t_captured_ns", C.c_int64), ("t_snapshot_ns", C.c_int64), ("t_persisted_ns", C.c_int64),
                 ("pack_ms", C.c_float), ("d2h_ms", C.c_float), ("kernel_launches", C.c_uint32),
                 ("copies", C.c_uint32), ("snapshot_done", C.c_int32), ("persisted_done", C.c_int32),
-                ("failed", C.c_int32), ("file_dma_bytes", C.c_uint64)]
+                ("failed", C.c_int32), ("file_dma_bytes", C.c_uint64),
+                ("host_checksum_bytes", C.c_uint64)]
 
 
 class RestoreObject(C.Structure):

@@ -14,6 +14,7 @@ moved by this library's kernels / DMA, never by PyTorch.
 from __future__ import annotations
 
 import ctypes as C
+import struct
 import os
 from dataclasses import dataclass, field
 from typing import Any, Dict, List, Optional
@@ -53,7 +54,15 @@ class Value:
 
     @staticmethod
     def from_py(v: Any) -> "Value":
-        return Value(_build(v))
+        # Fast path: canonical TLV bytes built in Python, one native decode
+        # (strict: invalid UTF-8, depth > 256 are rejected there). Anything
+        # unusual takes the element-by-element native builder.
+        try:
+            out = bytearray()
+            _enc_py(v, out, 0)
+            return Value.decode(bytes(out))
+        except (_Fallback, TsError):
+            return Value(_build(v))
 
     @staticmethod
     def metadata(rank_id, tp_idx, pp_idx, dp_idx, seed, metadata_bytes, iteration) -> "Value":
@@ -76,6 +85,71 @@ class Value:
 
     def to_py(self) -> Any:
         return _to_py(self.h)
+
+
+class _Fallback(Exception):
+    pass
+
+
+_U64 = struct.Struct("<Q")
+_I64 = struct.Struct("<q")
+_F64 = struct.Struct("<d")
+
+
+def _enc_py(v: Any, out: bytearray, depth: int) -> None:
+    """tlv::encode (tlv.cpp:39-77) of a plain Python value: tags 0 null,
+    1 int64, 2 f64, 3 utf8, 4 bytes, 5 list, 6 map (keys sorted, tagged strings)."""
+    if depth > 200:
+        raise _Fallback
+    if v is None:
+        out.append(0)
+    elif isinstance(v, bool):
+        raise _Fallback
+    elif isinstance(v, int):
+        if not -2**63 <= v < 2**64:
+            raise _Fallback
+        out.append(1)
+        out += _I64.pack(v if v < 2**63 else v - 2**64)
+    elif isinstance(v, float):
+        out.append(2)
+        out += _F64.pack(v)
+    elif isinstance(v, str):
+        try:
+            b = v.encode("utf-8")
+        except UnicodeEncodeError:
+            raise _Fallback
+        out.append(3)
+        out += _U64.pack(len(b))
+        out += b
+    elif isinstance(v, (bytes, bytearray, memoryview)):
+        b = bytes(v)
+        out.append(4)
+        out += _U64.pack(len(b))
+        out += b
+    elif isinstance(v, (list, tuple)):
+        out.append(5)
+        out += _U64.pack(len(v))
+        for x in v:
+            _enc_py(x, out, depth + 1)
+    elif isinstance(v, dict):
+        items = []
+        for k, x in v.items():
+            try:
+                items.append((str(k).encode("utf-8"), x))
+            except UnicodeEncodeError:
+                raise _Fallback
+        items.sort(key=lambda kv: kv[0])
+        if any(items[i][0] == items[i + 1][0] for i in range(len(items) - 1)):
+            raise _Fallback
+        out.append(6)
+        out += _U64.pack(len(items))
+        for kb, x in items:
+            out.append(3)
+            out += _U64.pack(len(kb))
+            out += kb
+            _enc_py(x, out, depth + 1)
+    else:
+        raise _Fallback
 
 
 def _build(v: Any) -> int:
@@ -259,6 +333,9 @@ class EngineConfig:
     pack_kernel: str = "warp"  # "warp" | "bulk" (TMA cp.async.bulk for large aligned fragments)
     bulk_min_bytes: int = 1 << 20
     file_dma: bool = True  # D2H straight into page-locked file pages when registered (rotation)
+    checksum_priority: int = -1  # RING device checksums' stream: 1 high, 0 normal, -1 low (default)
+    checksum_host_frac: float = -1.0  # share hashed by host workers: 0 all GPU, <0 auto (default)
+    ring_chunk_bytes: int = 0  # RING slot size without a full shadow (0 = auto: ring/6, <= 8 GiB)
 
     def to_c(self) -> N.EngineConfigC:
         c = N.EngineConfigC()
@@ -284,6 +361,9 @@ class EngineConfig:
         c.pack_kernel = {"warp": 0, "bulk": 1}[self.pack_kernel]
         c.bulk_min_bytes = self.bulk_min_bytes
         c.file_dma = int(self.file_dma)
+        c.checksum_priority = int(self.checksum_priority)
+        c.checksum_host_frac = float(self.checksum_host_frac)
+        c.ring_chunk_bytes = int(self.ring_chunk_bytes)
         return c
 
 

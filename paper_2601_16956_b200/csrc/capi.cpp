@@ -40,7 +40,7 @@ struct ts_engine {
   std::unique_ptr<engine> e;
 };
 struct ts_session {
-  std::unique_ptr<session> s;
+  std::shared_ptr<session> s;  // shared with the jobs issued on it
 };
 struct ts_ticket {
   std::shared_ptr<ticket_state> t;
@@ -198,6 +198,9 @@ void ts_engine_config_default(ts_engine_config* c) {
   c->pack_kernel = 0;
   c->bulk_min_bytes = 1ull << 20;
   c->file_dma = 1;
+  c->checksum_priority = -1;
+  c->checksum_host_frac = -1.0;
+  c->ring_chunk_bytes = 0;
 }
 
 ts_status ts_engine_create(const ts_engine_config* cfg, int rank_id, int device, ts_engine** out) {
@@ -242,7 +245,7 @@ ts_status ts_session_create(const char* dir, uint64_t checkpoint_id, uint64_t it
                             ts_session** out) {
   return guard([&] {
     auto* h = new ts_session;
-    h->s = std::make_unique<session>(dir ? dir : "", checkpoint_id, iteration, echo, n_ranks,
+    h->s = std::make_shared<session>(dir ? dir : "", checkpoint_id, iteration, echo, n_ranks,
                                      writes_manifest != 0);
     *out = h;
   });
@@ -289,7 +292,7 @@ ts_status ts_issue(ts_engine* e, ts_session* s, const ts_rank_info* rank, const 
                    size_t n, uint64_t iteration, void* producer_stream, ts_ticket** out) {
   return guard([&] {
     if (!e || !s || !rank || (!objs && n)) fail(TS_ERR_INVALID_ARG, "ts_issue: null argument");
-    auto t = e->e->issue(*s->s, *rank, objs, n, iteration, static_cast<cudaStream_t>(producer_stream));
+    auto t = e->e->issue(s->s, *rank, objs, n, iteration, static_cast<cudaStream_t>(producer_stream));
     *out = new ts_ticket{std::move(t)};
   });
 }
@@ -350,6 +353,7 @@ ts_status ts_ticket_stats_get(ts_ticket* t, ts_ticket_stats* o) {
     o->persisted_done = s.persisted;
     o->failed = s.failed;
     o->file_dma_bytes = s.file_dma_bytes;
+    o->host_checksum_bytes = s.host_checksum_bytes;
   });
 }
 

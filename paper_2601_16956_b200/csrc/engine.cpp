@@ -205,6 +205,7 @@ struct job {
     uint64_t file_off = 0, size = 0, img = 0;
     const uint8_t* src = nullptr;
     bool device = true;
+    bool gpu_ck = false;  // hashed by the FNV kernels (else by host workers)
     // checksum actor state (pieces arrive in object order)
     uint64_t fnv = fnv_seed, hashed = 0;
     bool busy = false, queued = false;
@@ -258,7 +259,7 @@ struct job {
     uint64_t ck = 0;
   };
 
-  session* sess = nullptr;
+  std::shared_ptr<session> sess;  // outlives the handle the caller may drop (engine.cpp:124 is a raw pointer)
   std::shared_ptr<ticket_state> t;
   int rank_id = 0;
   uint64_t iteration = 0;
@@ -273,6 +274,7 @@ struct job {
   std::deque<uint32_t> ready;  // host-hashed objects with landed, unhashed pieces
   std::vector<dev::seg> segs;
   std::vector<cudaEvent_t> chunk_events;  // per-job, destroyed at the end
+  std::vector<cudaEvent_t> ck_events;     // RING: checksums of chunk c done
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pack_events;  // kernel-only pack timing
   uint64_t img = 0;
   uint64_t win_bytes = 0;  // D2H window size W: windows are cut at multiples of W
@@ -283,7 +285,7 @@ struct job {
   // direct, zero-copy): files interleaved in proportion to their size, so the
   // flushers fill every file concurrently from the first window on.
   std::vector<uint32_t> worder;
-  bool gpu_ck = false;
+  bool gpu_ck = false, host_ck = false;
   std::vector<uint32_t> fnv_objs;
   uint64_t* fnv_out = nullptr;  // engine's mapped results buffer
   cudaEvent_t fnv_ev = nullptr;
@@ -292,6 +294,8 @@ struct job {
     for (auto& f : files)  // a claimed file that never finalized: its pages may be stale
       if (f.claimed && !f.released) file_registry::get().release(f.key, -1, false);
     for (auto e : chunk_events)
+      if (e) cudaEventDestroy(e);
+    for (auto e : ck_events)
       if (e) cudaEventDestroy(e);
     for (auto& pe : pack_events) {
       cudaEventDestroy(pe.first);
@@ -343,7 +347,12 @@ engine::engine(const ts_engine_config& cfg, int rank_id, int device)
   const int pack_prio = cfg_.pack_priority > 0 ? hi_prio : cfg_.pack_priority < 0 ? lo_prio : 0;
   cuda_check(cudaStreamCreateWithPriority(&pack_stream_, cudaStreamNonBlocking, pack_prio), "stream");
   cuda_check(cudaStreamCreateWithPriority(&copy_stream_, cudaStreamNonBlocking, lo_prio), "stream");
+  // RING checksums read the staged copy, not the state: they are off the
+  // capture path and may run at a lower priority than the pack.
+  const int ck_prio = cfg_.checksum_priority > 0 ? hi_prio : cfg_.checksum_priority < 0 ? lo_prio : 0;
+  cuda_check(cudaStreamCreateWithPriority(&ck_stream_, cudaStreamNonBlocking, ck_prio), "stream");
   workers_ = std::make_unique<thread_pool>(cfg_.flush_workers);
+  host_rate_ = 1.2e9 * cfg_.flush_workers;  // until measured: ~1.2 GB/s per worker (4 interleaved chains)
   copier_ = std::thread([this] { copier_loop(); });
   completer_ = std::thread([this] { completer_loop(); });
 }
@@ -356,6 +365,7 @@ engine::~engine() {
   if (fnvbuf_) cudaFree(fnvbuf_);
   if (ck_host_) cudaFreeHost(ck_host_);
   if (pack_stream_) cudaStreamDestroy(pack_stream_);
+  if (ck_stream_) cudaStreamDestroy(ck_stream_);
   if (copy_stream_) cudaStreamDestroy(copy_stream_);
   for (auto e : ev_free_) cudaEventDestroy(e);
 }
@@ -435,10 +445,32 @@ void* engine::ensure_seg_buffer(uint64_t bytes) {
 }
 
 // issue_checkpoint (engine.cpp:518-619), lazy by default.
-std::shared_ptr<ticket_state> engine::issue(session& s, const ts_rank_info& rank,
+std::shared_ptr<ticket_state> engine::issue(const std::shared_ptr<session>& sp, const ts_rank_info& rank,
                                             const ts_object_desc* objs, size_t n,
                                             uint64_t iteration, cudaStream_t producer) {
+  session& s = *sp;
   const int64_t t0 = now_ns();
+  if (last_job_) {
+    // Host slack of the checkpoint cadence: time from the previous checkpoint's
+    // persist to this issue (EMA). ~0 when the caller waits for persist before
+    // issuing again (closed loop), large when checkpoints are spaced by
+    // training steps; forgotten after a long pause.
+    int64_t prev_issue = 0, prev_persist = -1;
+    {
+      std::lock_guard<std::mutex> g(last_job_->t->mu);
+      prev_issue = last_job_->t->t_issue;
+      prev_persist = last_job_->t->persisted ? last_job_->t->t_persisted : -1;
+    }
+    const double gap = prev_persist < 0 ? 0.0 : static_cast<double>(t0 - prev_issue - prev_persist) / 1e9;
+    // (drops at once when the host fell behind, grows slowly)
+    slack_s_ = gap > 120 ? 0 : gap < slack_s_ ? std::max(0.0, gap) : 0.75 * slack_s_ + 0.25 * gap;
+  }
+  if (hash_bytes_.load() > (256ull << 20)) {  // host hashing rate of the previous jobs
+    const double per_thread = static_cast<double>(hash_bytes_.load()) / std::max<double>(1, hash_busy_ns_.load()) * 1e9;
+    host_rate_ = 0.9 * per_thread * cfg_.flush_workers;
+    hash_bytes_ = 0;
+    hash_busy_ns_ = 0;
+  }
   // One consistent device view at a time (engine.cpp:523-525).
   if (cfg_.strategy == TS_STRATEGY_LAZY && last_job_) {
     auto prev = last_job_->t;
@@ -449,7 +481,7 @@ std::shared_ptr<ticket_state> engine::issue(session& s, const ts_rank_info& rank
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
 
   auto j = std::make_shared<job>();
-  j->sess = &s;
+  j->sess = sp;
   j->rank_id = rank.rank_id;
   j->iteration = iteration;
   j->io = cfg_.write_files != 0;
@@ -547,9 +579,41 @@ std::shared_ptr<ticket_state> engine::issue(session& s, const ts_rank_info& rank
   }
 
   j->gpu_ck = cfg_.checksum_on_gpu != 0;
-  if (j->gpu_ck)
-    for (size_t k = 0; k < j->raws.size(); ++k)
-      if (j->raws[k].device) j->fnv_objs.push_back(static_cast<uint32_t>(k));
+  if (j->gpu_ck) {
+    // Checksum placement: the host workers take a
+    // share of the device-tier objects (spread evenly over the image, only
+    // objects one host chain finishes within the budget), the FNV kernels the
+    // rest. The share is fixed (checksum_host_frac >= 0) or sized so the host
+    // keeps up with the checkpoint cadence at its measured rate (< 0, auto).
+    uint64_t dev_bytes = 0;
+    for (const auto& r : j->raws) dev_bytes += r.device ? r.size : 0;
+    double frac = cfg_.checksum_host_frac;
+    double obj_cap = 1e30;
+    if (frac < 0) {
+      // host hashing overlaps the D2H; it may also use the slack before the
+      // next checkpoint, never delay persist beyond it
+      const double d2h_s = static_cast<double>(j->img) / 50e9;
+      const double budget_s = d2h_s + slack_s_;
+      frac = dev_bytes ? std::min(1.0, 0.8 * host_rate_ * budget_s / static_cast<double>(dev_bytes)) : 0.0;
+      obj_cap = 0.8 * chain_rate_ * budget_s;
+    }
+    uint64_t seen = 0, host = 0;
+    for (size_t k = 0; k < j->raws.size(); ++k) {
+      auto& r = j->raws[k];
+      if (!r.device) continue;
+      seen += r.size;
+      const bool to_host = frac > 0 && static_cast<double>(r.size) <= obj_cap &&
+                           static_cast<double>(host + r.size) <= frac * static_cast<double>(seen) + 0.5;
+      if (to_host) {
+        host += r.size;
+      } else {
+        r.gpu_ck = true;
+        j->fnv_objs.push_back(static_cast<uint32_t>(k));
+      }
+    }
+    t->host_checksum_bytes = host;
+    j->host_ck = host > 0;
+  }
 
   // D2H windows over [0, img) and their pieces (one sweep).
   const uint64_t W = std::min<uint64_t>(cfg_.raw_chunk_bytes, pool_->capacity());
@@ -600,7 +664,7 @@ std::shared_ptr<ticket_state> engine::issue(session& s, const ts_rank_info& rank
       key[k] = {frac, static_cast<uint32_t>(k)};
     }
     // Host-hashed pieces must reach their checksum actor in object order.
-    const bool host_hashed = !cfg_.checksum_on_gpu || !j->hp.empty();
+    const bool host_hashed = !cfg_.checksum_on_gpu || j->host_ck || !j->hp.empty();
     if (!host_hashed) std::stable_sort(key.begin(), key.end());
     for (const auto& kv : key) j->worder.push_back(kv.second);
   }
@@ -767,7 +831,12 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       chunk = want;
       nslots = 1;
     } else {
-      chunk = std::max<uint64_t>(W, std::min<uint64_t>(1ull << 30, cap / 2) / W * W);
+      // Few large chunks: every pack launch after the first ring-full waits
+      // for a free slot and then interrupts the training kernels once (at
+      // high priority), so fewer, larger launches interfere less.
+      const uint64_t want_chunk = cfg_.ring_chunk_bytes ? cfg_.ring_chunk_bytes
+                                                        : std::min<uint64_t>(8ull << 30, cap / 6);
+      chunk = std::max<uint64_t>(W, std::min<uint64_t>(want_chunk, cap / 2) / W * W);
       nslots = static_cast<size_t>(cap / chunk);
     }
     nchunks = (j->img + chunk - 1) / chunk;
@@ -876,7 +945,7 @@ void engine::run_job(const std::shared_ptr<job>& j) {
   // Launch k of the checksum kernels; the last one publishes the results
   // straight into the mapped pool region (a cudaMemcpy would queue behind the
   // bulk D2H windows on the copy engine).
-  auto launch_checksums = [&](size_t k) {
+  auto launch_checksums = [&](size_t k, cudaStream_t cs) {
     if (!nf || cbeg[k + 1] == cbeg[k]) {
       if (nf && k + 2 == cbeg.size()) goto publish;
       return;
@@ -886,13 +955,13 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&out), j->fnv_out, 0), "cudaHostGetDevicePointer");
       dev::launch_fnv(reinterpret_cast<dev::fnv_obj*>(fbuf) + cbeg[k], static_cast<uint32_t>(cbeg[k + 1] - cbeg[k]),
                       cdims[k].first, cdims[k].second, reinterpret_cast<uint64_t*>(fbuf + ftb), fbuf + ftb + fsb,
-                      pack_stream_, out);
+                      cs, out);
       t.kernel_launches += 11;
       cuda_check(cudaGetLastError(), "checksum kernels");
     }
     if (k + 2 != cbeg.size()) return;
   publish:
-    cuda_check(cudaEventRecord(j->fnv_ev, pack_stream_), "event");
+    cuda_check(cudaEventRecord(j->fnv_ev, cs), "event");
     {
       std::lock_guard<std::mutex> g(mu_);
       inflight_.push_back({j, 0, true});
@@ -903,7 +972,7 @@ void engine::run_job(const std::shared_ptr<job>& j) {
   cuda_check(cudaStreamWaitEvent(copy_stream_, t.ev_start, 0), "wait producer");
   cuda_check(cudaEventRecord(t.ev_pack0, mode == TS_D2H_DIRECT ? copy_stream_ : pack_stream_), "event");
   if (nf && !use_ring) {
-    launch_checksums(0);
+    launch_checksums(0, pack_stream_);
     // DIRECT captures on the copy stream: it must also cover the checksum reads.
     cuda_check(cudaStreamWaitEvent(copy_stream_, j->fnv_ev, 0), "wait checksums");
   }
@@ -916,12 +985,16 @@ void engine::run_job(const std::shared_ptr<job>& j) {
   if (mode == TS_D2H_RING) {
     const bool shadow = nslots == 1;
     j->chunk_events.assign(nchunks, nullptr);
+    j->ck_events.assign(nchunks, nullptr);
     size_t w = 0;
     cuda_check(cudaEventRecord(t.ev_d2h_first, copy_stream_), "event");
     for (size_t c = 0; c < nchunks && !failed(); ++c) {
       const uint64_t clo = c * chunk, chi = std::min(j->img, clo + chunk);
       uint8_t* slot = ring + (shadow ? 0 : (c % nslots) * chunk);
-      if (c >= nslots) cuda_check(cudaStreamWaitEvent(pack_stream_, j->chunk_events[c - nslots], 0), "slot wait");
+      if (c >= nslots) {  // the slot's previous chunk must have left the device and been checksummed
+        cuda_check(cudaStreamWaitEvent(pack_stream_, j->chunk_events[c - nslots], 0), "slot wait");
+        if (nf) cuda_check(cudaStreamWaitEvent(pack_stream_, j->ck_events[c - nslots], 0), "slot wait");
+      }
       cudaEvent_t pa, pb;
       cuda_check(cudaEventCreate(&pa), "event");
       cuda_check(cudaEventCreate(&pb), "event");
@@ -946,8 +1019,18 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       cuda_check(cudaEventRecord(packed, pack_stream_), "event");
       if (c + 1 == nchunks) mark_capture(pack_stream_);
       cuda_check(cudaStreamWaitEvent(copy_stream_, packed, 0), "wait pack");
-      cudaEventDestroy(packed);  // destruction is deferred until the event completes
-      if (nf) launch_checksums(c);  // reads the slot, overlaps the D2H; next pack of the slot queues behind
+      struct ev_guard {  // destruction is deferred until the event completes
+        cudaEvent_t e;
+        ~ev_guard() { cudaEventDestroy(e); }
+      } packed_guard{packed};
+      if (nf) {  // reads the slot on the checksum stream, overlapping the D2H
+        cuda_check(cudaStreamWaitEvent(ck_stream_, packed, 0), "wait pack");
+        launch_checksums(c, ck_stream_);
+        cudaEvent_t ck;
+        cuda_check(cudaEventCreateWithFlags(&ck, cudaEventDisableTiming), "event");
+        cuda_check(cudaEventRecord(ck, ck_stream_), "event");
+        j->ck_events[c] = ck;
+      }
       for (size_t q = w; q < j->wins.size() && j->wins[q].lo < chi; ++q, ++w) {
         const size_t wi = shadow ? j->worder[q] : q;
         auto& win = j->wins[wi];
@@ -972,6 +1055,14 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       j->chunk_events[c] = done;
     }
     cuda_check(cudaEventRecord(t.ev_d2h_last, copy_stream_), "event");
+    // later jobs reuse the ring and the checksum scratch: order them after these checksums
+    if (nf) {
+      cudaEvent_t tail;
+      cuda_check(cudaEventCreateWithFlags(&tail, cudaEventDisableTiming), "event");
+      cuda_check(cudaEventRecord(tail, ck_stream_), "event");
+      cuda_check(cudaStreamWaitEvent(pack_stream_, tail, 0), "wait checksums");
+      cudaEventDestroy(tail);
+    }
   } else if (mode == TS_D2H_ZEROCOPY) {
     uint8_t* dbase = nullptr;
     cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dbase), pool_->base(), 0),
@@ -1090,7 +1181,7 @@ void engine::window_landed(const std::shared_ptr<job>& j, size_t wi) {
       for (uint32_t k = w.fs_begin; k < w.fs_end; ++k) j->files[j->fs[k].f].win_pending -= 1;
     for (uint32_t k = w.wp_begin; k < w.wp_end; ++k) {
       auto& r = j->raws[j->wp[k].obj];
-      if (j->gpu_ck && r.device) continue;  // checksummed on the device
+      if (r.gpu_ck) continue;  // checksummed on the device
       w.refs += 1;
       r.q.push_back({base + j->wp[k].win_off, j->wp[k].len, static_cast<uint32_t>(wi)});
       if (!r.busy && !r.queued) {
@@ -1215,6 +1306,8 @@ void engine::hash_task(const std::shared_ptr<job>& j, size_t) {
       }
     }
     if (m == 0) return;
+    const int64_t hs = now_ns();
+    uint64_t hb = 0;
     uint64_t h[4];
     size_t pi[4] = {0, 0, 0, 0};
     uint64_t off[4] = {0, 0, 0, 0};
@@ -1234,6 +1327,7 @@ void engine::hash_task(const std::shared_ptr<job>& j, size_t) {
         hh[q] = h[k];
       }
       fnv_lockstep(ptr, hh, na, n);
+      hb += n * static_cast<uint64_t>(na);
       for (int q = 0; q < na; ++q) {
         const int k = act[q];
         h[k] = hh[q];
@@ -1244,6 +1338,8 @@ void engine::hash_task(const std::shared_ptr<job>& j, size_t) {
         }
       }
     }
+    hash_bytes_ += hb;
+    hash_busy_ns_ += static_cast<uint64_t>(now_ns() - hs);
     for (int k = 0; k < m; ++k) {
       auto& r = j->raws[ids[k]];
       uint64_t len = 0;

@@ -94,6 +94,7 @@ struct ticket_state {
   int64_t issue_block_ns = 0, barrier_block_ns = 0;
   uint64_t total_bytes = 0, raw_bytes = 0, serialized_bytes = 0, image_bytes = 0;
   uint64_t file_dma_bytes = 0;  // fixed-region bytes DMA'd straight into file pages
+  uint64_t host_checksum_bytes = 0;  // device-tier bytes hashed by host workers (rest: FNV kernels)
   float pack_ms = 0, d2h_ms = 0;
   uint32_t kernel_launches = 0, copies = 0;
   cudaEvent_t ev_start = nullptr, ev_capture = nullptr, ev_d2h_first = nullptr,
@@ -113,7 +114,7 @@ class engine {
  public:
   engine(const ts_engine_config& cfg, int rank_id, int device);
   ~engine();
-  std::shared_ptr<ticket_state> issue(session& s, const ts_rank_info& rank,
+  std::shared_ptr<ticket_state> issue(const std::shared_ptr<session>& s, const ts_rank_info& rank,
                                       const ts_object_desc* objs, size_t n, uint64_t iteration,
                                       cudaStream_t producer);
   // host_block: 0 = stream wait on the capture event (no host block), 1 = host
@@ -148,7 +149,7 @@ class engine {
   int rank_id_, device_, sms_;
   std::unique_ptr<pinned_pool> pool_;
   std::unique_ptr<thread_pool> workers_;
-  cudaStream_t pack_stream_ = nullptr, copy_stream_ = nullptr;
+  cudaStream_t pack_stream_ = nullptr, copy_stream_ = nullptr, ck_stream_ = nullptr;
   uint8_t* ring_ = nullptr;
   uint64_t ring_bytes_ = 0;
   void* segbuf_ = nullptr;
@@ -173,6 +174,9 @@ class engine {
   bool stopping_ = false, copier_done_ = false;
   std::shared_ptr<job> last_job_;
   std::string spare_dir_;  // recycled files of retired checkpoints (retire_checkpoint)
+  // checksum placement (auto): host hashing capacity, measured per job
+  double host_rate_ = 0, chain_rate_ = 0.45e9, slack_s_ = 0;
+  std::atomic<uint64_t> hash_bytes_{0}, hash_busy_ns_{0};
   std::thread copier_, completer_;
 };
 

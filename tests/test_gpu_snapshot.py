@@ -205,3 +205,23 @@ def test_retired_checkpoint_is_not_restorable(gpu, tmp_path):
     with pytest.raises(api.FormatError) as ei:
         api.restore_checkpoint(os.path.join(d, "MANIFEST.tlv"))
     assert ei.value.kind == "missing_file"
+
+
+@pytest.mark.parametrize("frac", [0.0, 0.3, 0.5, 1.0])
+@pytest.mark.parametrize("mode", ["ring", "direct", "zerocopy"])
+@pytest.mark.parametrize("name", ["hand_mixed", "zero3_tiny", "two_ranks"])
+def test_checksum_split_identical(gpu, tmp_path, name, mode, frac):
+    """Checksum placement split between the FNV kernels and host workers
+    (checksum_host_frac) writes the same bytes; the host share is honoured."""
+    rec = S.load_recipe(os.path.join(GOLDEN, "recipes", name + ".recipe"))
+    out = str(tmp_path / "ckpt")
+    _, _, stats, _ = checkpoint_recipe(rec, out, cfg_for(mode, checksum_host_frac=frac))
+    assert read_tree(out) == read_tree(os.path.join(GOLDEN, "trees", name))
+    dev = sum(o.size for r in rec.ranks for o in r.objects if o.kind == 0 and o.tier == 0)
+    host = sum(s["host_checksum_bytes"] for s in stats)
+    if frac == 0.0:
+        assert host == 0
+    elif frac == 1.0:
+        assert host == dev
+    else:
+        assert 0 <= host <= dev
