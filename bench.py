@@ -54,7 +54,7 @@ class Clocks:
                 ["nvidia-smi", "-i", str(self.dev), "--query-gpu=clocks.sm,clocks.max.sm,utilization.gpu,"
                  "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                 "clocks_event_reasons.sw_power_cap,power.draw", "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except Exception:
@@ -77,8 +77,15 @@ class Clocks:
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({n for s in self.samples for n, v in zip(names, s[4:8]) if v.lower() == "active"})
+        pw = []
+        for s in self.samples:
+            try:
+                pw.append(float(s[8]))
+            except (IndexError, ValueError):
+                pass
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w": round(statistics.median(pw), 1) if pw else None}
 
 
 def ncu_traffic(cfg: str, mode: str, pack_kernel: str):
@@ -251,8 +258,10 @@ def ours(args):
                            flush_workers=args.flush_workers or min(16, os.cpu_count() or 8), write_files=False,
                            checksum_on_gpu=not args.host_checksum, pack_kernel=args.pack_kernel,
                            checksum_priority=args.ck_priority, pack_priority=args.pack_priority,
-                           checksum_host_frac=args.ck_host_frac, ring_chunk_bytes=int(args.ring_chunk_gb * (1 << 30)))
+                           checksum_host_frac=args.ck_host_frac, ring_chunk_bytes=int(args.ring_chunk_gb * (1 << 30)),
+                           worker_nice=args.worker_nice)
     eng = api.CheckpointEngine(cfg, spec.rank_id, local_dev)
+    numa_node = eng.numa_node
     full = getattr(rec, "full_layout", None)
     echo = S.Recipe(layout=full).manifest_echo() if full else rec.manifest_echo()
     tdir = os.path.join("/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir(), "ts_bench")
@@ -450,7 +459,7 @@ def ours(args):
                        "checksums": "host" if args.host_checksum else "gpu", "pack_kernel": args.pack_kernel,
                        "priorities": {"pack": args.pack_priority, "checksums": args.ck_priority},
                        "checksum_host_frac": "auto" if args.ck_host_frac < 0 else args.ck_host_frac,
-                       "l2": "inputs > L2 (126 MB)",
+                       "numa_node": numa_node, "l2": "inputs > L2 (126 MB)",
                        "step": "update(pattern kernel) + issue + snapshot + checksums (no files)"},
             "per_gpu_gbps": round(value / ws, 3),
             "snapshot_ms_mean": round(statistics.mean(snap_ms), 2),
@@ -502,13 +511,19 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
     comp = torch.cuda.current_stream()
     res = {"off": ([], []), "lazy": ([], [])}
     host_ck = []
+    clk = {"off": [], "lazy": []}
+    fb_gpu = {"off": [], "lazy": []}  # CUDA-event time of fwd+bwd on the compute stream
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    rot_wait = []
     it = it0
 
     def rotate_and_issue(it):
+        tw = time.perf_counter()
         while len(ckpts) >= max(1, args.keep):  # rotation (a deployment does this off-thread)
             d0, _, t0k = ckpts.pop(0)
             t0k.wait_persisted()
             api.retire_checkpoint(d0, spare)
+        rot_wait.append(time.perf_counter() - tw)
         d = os.path.join(tdir, f"ckpt_{it:06d}")
         sess = api.CheckpointSession(d, it, it, None, 1, writes_manifest=True)
         return d, sess
@@ -525,15 +540,22 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
         t_end = time.time() + 120
         while api.file_cache_bytes() < want * min(max(1, args.keep), len(ckpts)) and time.time() < t_end:
             time.sleep(0.2)
+        rot_wait.clear()
     # off/lazy blocks alternate (twice) so clock / power-cap drift hits both arms
     for mode in ("off", "lazy", "off", "lazy"):
         pending = None
         times, blocked = res[mode]
+        sampler = Clocks(local)
+        sampler.__enter__()
         for k in range(args.train_steps + 1):
             comp.synchronize()  # like a per-step loss.item(): the compute stream only, never the device
             t0 = time.perf_counter()
+            ev0.record(comp)
             run()                                    # forward + backward
+            ev1.record(comp)
             comp.synchronize()  # fwd/bwd done (the simulator's synchronous phases, simulator.cpp:129-130)
+            if k > 0:
+                fb_gpu[mode].append(ev0.elapsed_time(ev1))
             b = eng.pre_update_barrier(pending, stream=comp, host_block=1) if pending else 0
             it += 1
             api.mutate_update_step(state, it, stream=comp)  # optimizer update
@@ -557,6 +579,8 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
                     blocked.append(1e3 * (b / 1e9 + ib))
                 elif b and blocked:
                     blocked[-1] += 1e3 * b / 1e9  # barrier wait attributed to its checkpoint
+        sampler.__exit__()
+        clk[mode].append(sampler.summary())
         if pending:
             pending.wait_persisted()
     res = {m: (statistics.mean(t), statistics.mean(b) if b else 0.0) for m, (t, b) in res.items()}
@@ -572,6 +596,10 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
             "slowdown_pct": round(100 * (lazy - off) / off, 2),
             "blocked_ms_per_ckpt": round(res["lazy"][1], 3),
             "host_checksum_frac": round(statistics.mean(host_ck), 3) if host_ck else None,
+            "rotation_wait_ms": round(1e3 * statistics.mean(rot_wait), 2) if rot_wait else None,
+            "fwd_bwd_gpu_ms": {m: round(statistics.mean(v), 1) for m, v in fb_gpu.items() if v},
+            "clocks": {m: {"sm_mhz": [c["sm_mhz"] for c in v], "power_w": [c.get("power_w") for c in v],
+                           "reasons": sorted({r for c in v for r in c["reasons"]})} for m, v in clk.items()},
             "checkpoints_to": (f"files on /dev/shm, rotation keeps {args.keep}, file_dma bytes of the last "
                                f"{len(dma)}: {dma}") if files else "snapshot only (pinned pool)"}
 
@@ -605,6 +633,7 @@ def main():
     ap.add_argument("--ring-gb", type=float, default=0.0,
                     help="HBM staging ring when no full device shadow fits (0 = auto: free HBM - 26 GiB)")
     ap.add_argument("--ring-chunk-gb", type=float, default=0.0, help="ring slot size (0 = auto)")
+    ap.add_argument("--worker-nice", type=int, default=10, help="nice increment of engine worker threads")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)

@@ -193,6 +193,10 @@ typedef struct ts_engine_config {
                                        finish within that time only */
   uint64_t ring_chunk_bytes;        /* RING without a full shadow: bytes per ring slot (0 = auto:
                                        ring/6, at most 8 GiB; rounded to whole windows) */
+  int32_t numa_bind;                /* 1 (default): engine threads and the pinned pool on the GPU's
+                                       NUMA node (multi-socket hosts; no-op on one node) */
+  int32_t worker_nice;              /* nice increment of the worker threads (default 10: background
+                                       to the training process's launching thread); 0 = none */
 } ts_engine_config;
 
 void ts_engine_config_default(ts_engine_config* cfg);
@@ -202,6 +206,8 @@ void ts_engine_config_default(ts_engine_config* cfg);
 ts_status ts_engine_create(const ts_engine_config* cfg, int rank_id, int device, ts_engine** out);
 /* checkpoint_engine::shutdown (engine.cpp:213-234) + dtor */
 ts_status ts_engine_destroy(ts_engine* e);
+/* NUMA node the engine placed its threads and pinned pool on (-1: none / single node). */
+int ts_engine_numa_node(ts_engine* e);
 
 /* Manifest echo of a layout-based session (engine.cpp:35-54); NULL => defaults of
  * the n_ranks ctor (engine.cpp:56-66). */

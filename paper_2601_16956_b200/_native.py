@@ -102,7 +102,8 @@ class EngineConfigC(C.Structure):
                 ("pack_threads", C.c_int32), ("pack_priority", C.c_int32), ("write_files", C.c_int32),
                 ("checksum_on_gpu", C.c_int32), ("flush_mmap", C.c_int32), ("pack_kernel", C.c_int32),
                 ("bulk_min_bytes", C.c_uint64), ("file_dma", C.c_int32), ("checksum_priority", C.c_int32),
-                ("_pad2", C.c_int32), ("checksum_host_frac", C.c_double), ("ring_chunk_bytes", C.c_uint64)]
+                ("_pad2", C.c_int32), ("checksum_host_frac", C.c_double), ("ring_chunk_bytes", C.c_uint64),
+                ("numa_bind", C.c_int32), ("worker_nice", C.c_int32)]
 
 
 class ManifestEcho(C.Structure):
@@ -188,6 +189,7 @@ _sig("ts_engine_create", i32, C.POINTER(EngineConfigC), i32, i32, C.POINTER(P))
 _sig("ts_engine_destroy", i32, P)
 _sig("ts_retire_checkpoint", i32, C.c_char_p, C.c_char_p)
 _sig("ts_engine_set_spare_dir", i32, P, C.c_char_p)
+_sig("ts_engine_numa_node", i32, P)
 _sig("ts_file_cache_bytes", C.c_uint64)
 _sig("ts_file_cache_release_all", i32, C.POINTER(C.c_uint64))
 _sig("ts_session_create", i32, C.c_char_p, u64, u64, C.POINTER(ManifestEcho), i32, i32, C.POINTER(P))

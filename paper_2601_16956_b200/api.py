@@ -336,6 +336,8 @@ class EngineConfig:
     checksum_priority: int = -1  # RING device checksums' stream: 1 high, 0 normal, -1 low (default)
     checksum_host_frac: float = -1.0  # share hashed by host workers: 0 all GPU, <0 auto (default)
     ring_chunk_bytes: int = 0  # RING slot size without a full shadow (0 = auto: ring/6, <= 8 GiB)
+    numa_bind: bool = True  # engine threads + pinned pool on the GPU's NUMA node (multi-socket hosts)
+    worker_nice: int = 10  # nice increment of the background worker threads (0 = none)
 
     def to_c(self) -> N.EngineConfigC:
         c = N.EngineConfigC()
@@ -364,6 +366,8 @@ class EngineConfig:
         c.checksum_priority = int(self.checksum_priority)
         c.checksum_host_frac = float(self.checksum_host_frac)
         c.ring_chunk_bytes = int(self.ring_chunk_bytes)
+        c.numa_bind = int(self.numa_bind)
+        c.worker_nice = int(self.worker_nice)
         return c
 
 
@@ -523,6 +527,11 @@ class CheckpointEngine:
             sh = _stream_handle(stream)
         N.call(N.lib.ts_pre_update_barrier, self.h, ticket.h, C.c_void_p(sh), host_block, C.byref(ns))
         return ns.value
+
+    @property
+    def numa_node(self) -> int:
+        """NUMA node of the engine's threads and pinned pool (-1: none / single node)."""
+        return int(N.lib.ts_engine_numa_node(self.h))
 
     def set_spare_dir(self, spare_dir: str):
         """Take over files of checkpoints retired into `spare_dir` (retire_checkpoint)."""

@@ -201,6 +201,8 @@ void ts_engine_config_default(ts_engine_config* c) {
   c->checksum_priority = -1;
   c->checksum_host_frac = -1.0;
   c->ring_chunk_bytes = 0;
+  c->numa_bind = 1;
+  c->worker_nice = 10;
 }
 
 ts_status ts_engine_create(const ts_engine_config* cfg, int rank_id, int device, ts_engine** out) {
@@ -235,6 +237,8 @@ ts_status ts_file_cache_release_all(uint64_t* released_bytes) {
     if (released_bytes) *released_bytes = b;
   });
 }
+
+int ts_engine_numa_node(ts_engine* e) { return e && e->e ? e->e->numa_node() : -1; }
 
 ts_status ts_engine_destroy(ts_engine* e) {
   return guard([&] { delete e; });

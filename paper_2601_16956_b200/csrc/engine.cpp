@@ -1,7 +1,10 @@
 // B200 snapshot engine (see engine.hpp for the reference mapping).
 #include "engine.hpp"
 
+#include <sys/resource.h>
 #include <sys/stat.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cerrno>
@@ -45,9 +48,10 @@ std::chrono::steady_clock::time_point to_tp(int64_t ns) {
 // ---------------------------------------------------------------------------
 // thread pool
 
-thread_pool::thread_pool(int n) {
+thread_pool::thread_pool(int n, std::function<void()> init) {
   for (int i = 0; i < std::max(1, n); ++i)
-    threads_.emplace_back([this] {
+    threads_.emplace_back([this, init] {
+      if (init) init();
       for (;;) {
         std::function<void()> f;
         {
@@ -338,7 +342,11 @@ engine::engine(const ts_engine_config& cfg, int rank_id, int device)
     fail(TS_ERR_CUDA, "no CUDA device: the B200 engine has no CPU fallback");
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   sms_ = dev::sm_count(device_);
-  pool_ = std::make_unique<pinned_pool>(cfg_.staging_capacity_bytes);
+  if (cfg_.numa_bind) numa_ = numa_for_device(device_);
+  {
+    numa_prefer_scope near(numa_);  // pinned pool pages on the GPU's node
+    pool_ = std::make_unique<pinned_pool>(cfg_.staging_capacity_bytes);
+  }
   int lo_prio = 0, hi_prio = 0;
   cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
   // Capture kernels preempt compute at CTA granularity (high priority): at low
@@ -351,7 +359,14 @@ engine::engine(const ts_engine_config& cfg, int rank_id, int device)
   // capture path and may run at a lower priority than the pack.
   const int ck_prio = cfg_.checksum_priority > 0 ? hi_prio : cfg_.checksum_priority < 0 ? lo_prio : 0;
   cuda_check(cudaStreamCreateWithPriority(&ck_stream_, cudaStreamNonBlocking, ck_prio), "stream");
-  workers_ = std::make_unique<thread_pool>(cfg_.flush_workers);
+  // Workers (checksums, flushes, serialization, page locking) are background
+  // work: a lower CPU priority keeps the training process's kernel-launching
+  // thread responsive when every core is hashing.
+  const int nice_inc = cfg_.worker_nice;
+  workers_ = std::make_unique<thread_pool>(cfg_.flush_workers, [this, nice_inc] {
+    numa_bind_thread(numa_);
+    if (nice_inc > 0) setpriority(PRIO_PROCESS, static_cast<id_t>(syscall(SYS_gettid)), nice_inc);
+  });
   host_rate_ = 1.2e9 * cfg_.flush_workers;  // until measured: ~1.2 GB/s per worker (4 interleaved chains)
   copier_ = std::thread([this] { copier_loop(); });
   completer_ = std::thread([this] { completer_loop(); });
@@ -742,6 +757,7 @@ int64_t engine::pre_update_barrier(const std::shared_ptr<ticket_state>& t, cudaS
 
 void engine::copier_loop() {
   cudaSetDevice(device_);
+  numa_bind_thread(numa_);
   for (;;) {
     std::shared_ptr<job> j;
     {
@@ -1122,6 +1138,7 @@ void engine::run_job(const std::shared_ptr<job>& j) {
 
 void engine::completer_loop() {
   cudaSetDevice(device_);
+  numa_bind_thread(numa_);
   for (;;) {
     pending_window pw;
     {

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "filereg.hpp"
+#include "numa.hpp"
 #include "format.hpp"
 #include "kernels.cuh"
 
@@ -37,7 +38,8 @@ void cuda_check(cudaError_t e, const char* what);
 
 class thread_pool {
  public:
-  explicit thread_pool(int n);
+  // `init` runs first on every worker thread (e.g. NUMA binding)
+  explicit thread_pool(int n, std::function<void()> init = {});
   ~thread_pool();
   void submit(std::function<void()> f);
   int size() const { return static_cast<int>(threads_.size()); }
@@ -125,6 +127,7 @@ class engine {
   void set_spare_dir(const std::string& d) { spare_dir_ = d; }
   const ts_engine_config& config() const { return cfg_; }
   int device() const { return device_; }
+  int numa_node() const { return numa_.node; }
 
  private:
   friend struct job;
@@ -147,6 +150,7 @@ class engine {
 
   ts_engine_config cfg_;
   int rank_id_, device_, sms_;
+  numa_place numa_;  // the GPU's NUMA node: engine threads + pinned pool live there
   std::unique_ptr<pinned_pool> pool_;
   std::unique_ptr<thread_pool> workers_;
   cudaStream_t pack_stream_ = nullptr, copy_stream_ = nullptr, ck_stream_ = nullptr;
