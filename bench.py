@@ -186,8 +186,9 @@ def reference_arm(args):
     print(json.dumps(line))
 
 
-def gemm_load(ms: float, dev):
-    """Synthetic forward/backward: back-to-back bf16 GEMMs for ~ms milliseconds."""
+def gemm_load(ms: float, dev, graph: bool = False):
+    """Synthetic forward/backward: back-to-back bf16 GEMMs for ~ms milliseconds,
+    launched eagerly from Python or replayed as one CUDA graph."""
     import torch
 
     n = 8192
@@ -203,6 +204,19 @@ def gemm_load(ms: float, dev):
     e1.synchronize()
     per = e0.elapsed_time(e1) / 10
     reps = max(1, int(ms / per))
+    if graph:
+        c = torch.empty(n, n, device=dev, dtype=torch.bfloat16)
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                torch.matmul(a, b, out=c)
+        torch.cuda.current_stream().wait_stream(side)
+        with torch.cuda.graph(g):
+            for _ in range(reps):
+                torch.matmul(a, b, out=c)
+        return g.replay, reps * per
 
     def run():
         c = None
@@ -489,7 +503,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
     barrier_block, simulator.cpp:211-212) and the step-time slowdown."""
     import torch
 
-    run, fb_ms = gemm_load(args.fwd_bwd_ms, dev)
+    run, fb_ms = gemm_load(args.fwd_bwd_ms, dev, graph=args.fwd_bwd == "graph")
     # Checkpoints go where a deployment puts them: files on tmpfs with rotation
     # (keep `--keep`, file_dma), when tmpfs has room; else snapshot-only.
     ws, rank, _ = dist_info()
@@ -513,6 +527,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
     host_ck = []
     clk = {"off": [], "lazy": []}
     fb_gpu = {"off": [], "lazy": []}  # CUDA-event time of fwd+bwd on the compute stream
+    phases = {"off": [], "lazy": []}  # host wall per step phase
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     rot_wait = []
     it = it0
@@ -556,9 +571,12 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
             comp.synchronize()  # fwd/bwd done (the simulator's synchronous phases, simulator.cpp:129-130)
             if k > 0:
                 fb_gpu[mode].append(ev0.elapsed_time(ev1))
+            p_fb = time.perf_counter()
             b = eng.pre_update_barrier(pending, stream=comp, host_block=1) if pending else 0
+            p_bar = time.perf_counter()
             it += 1
             api.mutate_update_step(state, it, stream=comp)  # optimizer update
+            p_upd = time.perf_counter()
             ib = 0
             if mode == "lazy" and k % args.ckpt_interval == 0:
                 if files:
@@ -572,9 +590,12 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
                     ckpts.append((d, sess, pending))
                 if k > 0:
                     host_ck.append(pending.stats()["host_checksum_bytes"] / max(1, spec.raw_bytes))
+            p_iss = time.perf_counter()
             comp.synchronize()
             if k > 0:
-                times.append(time.perf_counter() - t0)
+                p_end = time.perf_counter()
+                times.append(p_end - t0)
+                phases[mode].append((p_fb - t0, p_bar - p_fb, p_upd - p_bar, p_iss - p_upd, p_end - p_iss))
                 if mode == "lazy" and k % args.ckpt_interval == 0:
                     blocked.append(1e3 * (b / 1e9 + ib))
                 elif b and blocked:
@@ -591,13 +612,17 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
         shutil.rmtree(tdir, ignore_errors=True)
         api.file_cache_release_all()
     off, lazy = res["off"][0], res["lazy"][0]
-    return {"fwd_bwd_ms": round(fb_ms, 1), "steps": 2 * args.train_steps, "ckpt_interval": args.ckpt_interval,
+    return {"fwd_bwd_ms": round(fb_ms, 1), "fwd_bwd_launch": args.fwd_bwd, "steps": 2 * args.train_steps,
+            "ckpt_interval": args.ckpt_interval,
             "step_ms_no_ckpt": round(1e3 * off, 2), "step_ms_lazy_ckpt": round(1e3 * lazy, 2),
             "slowdown_pct": round(100 * (lazy - off) / off, 2),
             "blocked_ms_per_ckpt": round(res["lazy"][1], 3),
             "host_checksum_frac": round(statistics.mean(host_ck), 3) if host_ck else None,
             "rotation_wait_ms": round(1e3 * statistics.mean(rot_wait), 2) if rot_wait else None,
             "fwd_bwd_gpu_ms": {m: round(statistics.mean(v), 1) for m, v in fb_gpu.items() if v},
+            "phase_ms": {m: dict(zip(["fwd_bwd", "barrier", "update_launch", "issue", "final_sync"],
+                                     [round(1e3 * statistics.mean(x), 2) for x in zip(*v)]))
+                         for m, v in phases.items() if v},
             "clocks": {m: {"sm_mhz": [c["sm_mhz"] for c in v], "power_w": [c.get("power_w") for c in v],
                            "reasons": sorted({r for c in v for r in c["reasons"]})} for m, v in clk.items()},
             "checkpoints_to": (f"files on /dev/shm, rotation keeps {args.keep}, file_dma bytes of the last "
@@ -615,6 +640,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--train-steps", type=int, default=3)
     ap.add_argument("--fwd-bwd-ms", type=float, default=1800.0)
+    ap.add_argument("--fwd-bwd", default="graph", choices=["graph", "eager"],
+                    help="synthetic fwd/bwd launched as one CUDA graph (default) or eagerly from Python")
     ap.add_argument("--ckpt-interval", type=int, default=1, help="checkpoint every k training steps")
     ap.add_argument("--host-checksum", action="store_true", help="FNV on host threads instead of the GPU kernels")
     ap.add_argument("--pack-kernel", default="warp", choices=["warp", "bulk"])

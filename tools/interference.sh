@@ -12,7 +12,7 @@ python - <<'PY'
 import json
 for l in open("gpurun_out/interference.jsonl"):
     d = json.loads(l); b = d["blocked"]; c = d["config"]
-    print(c["workload"][:5], c["checksums"], c.get("checksum_host_frac"), "interval", b["ckpt_interval"],
+    print(c["workload"][:5], b.get("fwd_bwd_launch"), c.get("checksum_host_frac"), "interval", b["ckpt_interval"],
           "slowdown %", b["slowdown_pct"], "blocked ms", b["blocked_ms_per_ckpt"], "host frac", b.get("host_checksum_frac"),
           "off", b["step_ms_no_ckpt"], "lazy", b["step_ms_lazy_ckpt"])
 PY
