@@ -420,6 +420,7 @@ def ours(args):
             in_place = False
         else:  # no room for a second copy of the shard (cfg4): restore into the state itself
             rs, in_place = state, True
+            r.restore_rank(ridx, local_dev, into=rs)  # warm-up (staging buffers), like the fresh case
         for o in rs.objects:  # zeroed destinations: a restore that skips bytes cannot pass
             if o.is_raw() and o.payload is not None:
                 o.payload.zero_()

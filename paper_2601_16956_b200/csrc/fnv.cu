@@ -9,13 +9,14 @@
 // The low byte is a T-function: its low nibble evolves on its own,
 // lo' = ((lo ^ b) * 3) mod 16, and the high nibble depends only on itself and
 // the known low-nibble trajectory. Hence three data passes per segment:
-//   A: 16-way speculation of the start low nibble  -> nibble map piA (64 bits)
+//   A: speculation of the start low nibble  -> nibble map piA (64 bits)
 //      (serial scan over segments fixes each segment's start low nibble)
-//   B: 16-way speculation of the start high nibble -> nibble map piB
+//   B: speculation of the start high nibble -> nibble map piB
 //      (serial scan fixes the start byte of every segment)
 //   C: Horner accumulation of C_seg with the known byte trajectory
-// and a final per-object combine. ~40 integer ops/byte, all lanes busy: the
-// checksum leaves the host cores free and costs a few ms of GPU per GB.
+// and a final per-object combine. Both nibble maps satisfy f(s^8) = f(s)^8, so
+// 8 candidates (two registers of 8-bit lanes) determine all 16. ~26 integer
+// ops/byte, all lanes busy.
 #include <cstdio>
 
 #include "kernels.cuh"
@@ -75,34 +76,70 @@ __device__ __forceinline__ seg_ref seg_of(const fnv_obj* o, uint32_t n, uint64_t
   return {o[i].ptr + off, umin64(sl, o[i].len - off)};
 }
 
-// Pass A: end low nibble for each of the 16 possible start low nibbles.
+// Visits [p, p+n) in order: f1(byte) for an unaligned head / tail, f4(word)
+// for each little-endian 32-bit word of the 16-B aligned body.
+template <class F1, class F4>
+__device__ __forceinline__ void for_words(const uint8_t* p, uint64_t n, F1&& f1, F4&& f4) {
+  uint64_t i = 0;
+  const uint64_t head = umin64(n, (16 - (reinterpret_cast<uintptr_t>(p) & 15)) & 15);
+  for (; i < head; ++i) f1(static_cast<uint32_t>(__ldg(p + i)));
+  const uint4* v = reinterpret_cast<const uint4*>(p + i);
+  const uint64_t nv = (n - i) >> 4;
+  for (uint64_t k = 0; k < nv; ++k) {
+    const uint4 w = __ldg(v + k);
+    f4(w.x);
+    f4(w.y);
+    f4(w.z);
+    f4(w.w);
+  }
+  for (i += nv * 16; i < n; ++i) f1(static_cast<uint32_t>(__ldg(p + i)));
+}
+
+// Both nibble automata satisfy f(s ^ 8) = f(s) ^ 8 (x*3 +- 24 = x*3 + 8 mod
+// 16, and the high nibble's carry-in does not depend on its own state), so a
+// segment's 16-entry nibble map is fixed by the end states of the starts 0..7:
+// map[s + 8] = map[s] ^ 8. Eight candidates = two registers of 8-bit lanes.
+__device__ __forceinline__ uint64_t nibble_map8(uint32_t v0, uint32_t v1) {
+  uint64_t m = 0;
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const uint32_t e = ((s < 4 ? v0 : v1) >> (8 * (s & 3))) & 15u;
+    m |= static_cast<uint64_t>(e) << (4 * s);
+    m |= static_cast<uint64_t>(e ^ 8u) << (4 * (s + 8));
+  }
+  return m;
+}
+
+// Pass A: end low nibble for each start low nibble (lo' = ((lo ^ b) * 3) mod 16).
 __global__ void __launch_bounds__(256) fnv_pass_a(const fnv_obj* __restrict__ o, uint32_t n, uint64_t nseg,
                                                   uint64_t* __restrict__ piA) {
   const uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (g >= nseg) return;
   uint32_t obj;
   const seg_ref s = seg_of(o, n, g, &obj);
-  uint32_t v0 = 0x03020100u, v1 = 0x07060504u, v2 = 0x0b0a0908u, v3 = 0x0f0e0d0cu;
-  for_bytes(s.p, s.len, [&](uint32_t b) {
-    const uint32_t bb = (b & 15u) * 0x01010101u;
+  uint32_t v0 = 0x03020100u, v1 = 0x07060504u;
+  auto step = [&](uint32_t bb) {  // bb: the byte's low nibble in every lane
     v0 = ((v0 ^ bb) * 3u) & 0x0f0f0f0fu;
     v1 = ((v1 ^ bb) * 3u) & 0x0f0f0f0fu;
-    v2 = ((v2 ^ bb) * 3u) & 0x0f0f0f0fu;
-    v3 = ((v3 ^ bb) * 3u) & 0x0f0f0f0fu;
-  });
-  const uint32_t v[4] = {v0, v1, v2, v3};
-  uint64_t m = 0;
-#pragma unroll
-  for (int s4 = 0; s4 < 16; ++s4) m |= static_cast<uint64_t>((v[s4 >> 2] >> (8 * (s4 & 3))) & 15u) << (4 * s4);
-  piA[g] = m;
+  };
+  for_words(
+      s.p, s.len, [&](uint32_t b) { step((b & 15u) * 0x01010101u); },
+      [&](uint32_t w) {
+        const uint32_t lw = w & 0x0f0f0f0fu;
+        step(__byte_perm(lw, 0, 0x0000));
+        step(__byte_perm(lw, 0, 0x1111));
+        step(__byte_perm(lw, 0, 0x2222));
+        step(__byte_perm(lw, 0, 0x3333));
+      });
+  piA[g] = nibble_map8(v0, v1);
 }
 
-// Pass B: with the start low nibble fixed, end high nibble for the 16 start
-// high nibbles. With x = l ^ b = 16*xh + xl and t = xl * 0xb3 (known once the
+// Pass B: with the start low nibble fixed, end high nibble for each start high
+// nibble. With x = l ^ b = 16*xh + xl and t = xl * 0xb3 (known once the
 // low-nibble trajectory is), the byte update splits into
-//     lo' = t mod 16,   hi' = (3*xh + (t >> 4)) mod 16,
-// i.e. 4-bit lanes: 16 candidates in four 32-bit registers, one LOP3 + one
-// IMAD per register per byte (no 16-bit lanes, no multiply by 0xb3 per lane).
+//     lo' = t mod 16,   hi' = (3*xh + (t >> 4)) mod 16.
+// Lanes hold 3*(v ^ bh) + (t >> 4) <= 45 + 167 < 256 before the mask, so the
+// carry-in needs no mask of its own.
 __global__ void __launch_bounds__(256) fnv_pass_b(const fnv_obj* __restrict__ o, uint32_t n, uint64_t nseg,
                                                   const uint8_t* __restrict__ lo_start,
                                                   uint64_t* __restrict__ piB) {
@@ -111,22 +148,24 @@ __global__ void __launch_bounds__(256) fnv_pass_b(const fnv_obj* __restrict__ o,
   uint32_t obj;
   const seg_ref s = seg_of(o, n, g, &obj);
   uint32_t lo = lo_start[g];
-  uint32_t v0 = 0x03020100u, v1 = 0x07060504u, v2 = 0x0b0a0908u, v3 = 0x0f0e0d0cu;
-  for_bytes(s.p, s.len, [&](uint32_t b) {
-    const uint32_t t = ((lo ^ b) & 15u) * 0xb3u;
+  uint32_t v0 = 0x03020100u, v1 = 0x07060504u;
+  auto step = [&](uint32_t bl, uint32_t bh) {  // bl: low nibble in bits 0-3; bh: high nibble, every lane
+    const uint32_t t = ((lo ^ bl) & 15u) * 0xb3u;
     lo = t & 15u;
-    const uint32_t c = ((t >> 4) & 15u) * 0x01010101u;
-    const uint32_t bh = (b >> 4) * 0x01010101u;
+    const uint32_t c = (t >> 4) * 0x01010101u;
     v0 = (((v0 ^ bh) * 3u) + c) & 0x0f0f0f0fu;
     v1 = (((v1 ^ bh) * 3u) + c) & 0x0f0f0f0fu;
-    v2 = (((v2 ^ bh) * 3u) + c) & 0x0f0f0f0fu;
-    v3 = (((v3 ^ bh) * 3u) + c) & 0x0f0f0f0fu;
-  });
-  const uint32_t v[4] = {v0, v1, v2, v3};
-  uint64_t m = 0;
-#pragma unroll
-  for (int s4 = 0; s4 < 16; ++s4) m |= static_cast<uint64_t>((v[s4 >> 2] >> (8 * (s4 & 3))) & 15u) << (4 * s4);
-  piB[g] = m;
+  };
+  for_words(
+      s.p, s.len, [&](uint32_t b) { step(b, (b >> 4) * 0x01010101u); },
+      [&](uint32_t w) {
+        const uint32_t hw = (w >> 4) & 0x0f0f0f0fu;
+        step(w, __byte_perm(hw, 0, 0x0000));
+        step(w >> 8, __byte_perm(hw, 0, 0x1111));
+        step(w >> 16, __byte_perm(hw, 0, 0x2222));
+        step(w >> 24, __byte_perm(hw, 0, 0x3333));
+      });
+  piB[g] = nibble_map8(v0, v1);
 }
 
 // Pass C: Horner sum C_seg = sum_i P^(k-1-i) D(x_i) with the known byte trajectory.
