@@ -438,6 +438,12 @@ def ours(args):
         e2e["restore_bit_exact"] = bad == 0
         e2e["restore_into"] = "the live state (zeroed first)" if in_place else "fresh, zeroed shards"
         e2e["restore_stats"] = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in r2.last_stats.items()}
+        um = r2.last_stats.get("unpack_ms", 0.0)
+        if um > 0:  # scatter-unpack kernel: reads the staged image, writes the shards (HBM roofline)
+            ub = 2 * raw
+            e2e["unpack_roofline"] = {"kernel": "unpack_kernel", "bound": "hbm", "achieved": round(ub / (um / 1e3) / 1e9, 1),
+                                      "peak": hbm_peak, "unit": "GB/s", "frac": round(ub / (um / 1e3) / 1e9 / hbm_peak, 3),
+                                      "alg_bytes": int(ub), "kernel_ms": round(um, 3)}
         del rs, r, r2
         eng_io.shutdown()
     else:

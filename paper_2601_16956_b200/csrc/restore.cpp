@@ -243,6 +243,16 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
   std::vector<host_cb_arg> cb_args(K);
   for (int k = 0; k < K; ++k) cb_args[k] = {&S, k};
   std::mutex cuda_mu;  // keeps each window's H2D + unpack + callback contiguous on the stream
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> unpack_ev;  // kernel-only unpack timing (roofline)
+  struct ev_list_guard {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v;
+    ~ev_list_guard() {
+      for (auto& e : v) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+      }
+    }
+  } unpack_ev_guard{unpack_ev};
   std::atomic<uint32_t> launches_a{0};
   const int ctas = dev::sm_count(device) * 2;
   auto set_err = [&](const error& e) {
@@ -274,7 +284,13 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
                                 [](const dev::useg& u, uint64_t x) { return u.pos + u.len <= x; });
     if (uit != usegs.end() && uit->pos < hi) {
       const size_t ui = static_cast<size_t>(uit - usegs.begin());
+      cudaEvent_t u0 = nullptr, u1 = nullptr;
+      cudaEventCreate(&u0);
+      cudaEventCreate(&u1);
+      cudaEventRecord(u0, st);
       dev::launch_unpack(d_usegs + ui, static_cast<uint32_t>(usegs.size() - ui), lo, hi, ds, ctas, 512, st);
+      cudaEventRecord(u1, st);
+      unpack_ev.emplace_back(u0, u1);
       launches_a += 1;
       cuda_check(cudaGetLastError(), "unpack launch");
     }
@@ -400,6 +416,11 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
   (void)d_states;
   float h2d_ms = 0;
   cudaEventElapsedTime(&h2d_ms, ev_a, ev_b);
+  float unpack_ms = 0;
+  for (auto& ue : unpack_ev) {
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, ue.first, ue.second) == cudaSuccess) unpack_ms += ms;
+  }
   cudaEventDestroy(ev_a);
   cudaEventDestroy(ev_b);
 
@@ -445,7 +466,7 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
     stats->verify_s = (now_ns() - t_verify) * 1e-9;
     stats->h2d_unpack_s = h2d_ms * 1e-3;
     stats->h2d_ms = h2d_ms;
-    stats->unpack_ms = 0;
+    stats->unpack_ms = unpack_ms;
     stats->total_s = (now_ns() - t_begin) * 1e-9;
     stats->kernel_launches = launches;
   }
