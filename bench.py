@@ -421,21 +421,38 @@ def ours(args):
         else:  # no room for a second copy of the shard (cfg4): restore into the state itself
             rs, in_place = state, True
             r.restore_rank(ridx, local_dev, into=rs)  # warm-up (staging buffers), like the fresh case
+        for o, so in zip(rs.objects, spec.objects):  # what pattern_mismatches checks against
+            o.pattern_space, o.pattern_offset = so.space, so.offset
+        rs.seed = spec.seed
         for o in rs.objects:  # zeroed destinations: a restore that skips bytes cannot pass
             if o.is_raw() and o.payload is not None:
                 o.payload.zero_()
         torch.cuda.synchronize()
+        # cold path (a restart: pread -> pinned -> H2D), then in-process
+        # rollback (the files this process page-locked: H2D from the page cache)
         t0 = time.time()
-        r2 = api.Restorer(man)
+        r2 = api.Restorer(man, use_file_cache=False)
         r2.restore_rank(ridx, local_dev, into=rs)
         torch.cuda.synchronize()
         restore_s = time.time() - t0
+        bad_cold = api.pattern_mismatches(rs, it)
+        for o in rs.objects:
+            if o.is_raw() and o.payload is not None:
+                o.payload.zero_()
+        torch.cuda.synchronize()
+        t0 = time.time()
+        r3 = api.Restorer(man)
+        r3.restore_rank(ridx, local_dev, into=rs)
+        torch.cuda.synchronize()
+        restore_warm_s = time.time() - t0
         for o, so in zip(rs.objects, spec.objects):
             o.pattern_space, o.pattern_offset = so.space, so.offset
         rs.seed = spec.seed
         bad = api.pattern_mismatches(rs, it)
         e2e["restore_gbps"] = round(raw / restore_s / 1e9, 3)
-        e2e["restore_bit_exact"] = bad == 0
+        e2e["restore_warm_gbps"] = round(raw / restore_warm_s / 1e9, 3)
+        e2e["restore_warm_direct_bytes"] = int(r3.last_stats.get("direct_bytes", 0))
+        e2e["restore_bit_exact"] = bad == 0 and bad_cold == 0
         e2e["restore_into"] = "the live state (zeroed first)" if in_place else "fresh, zeroed shards"
         e2e["restore_stats"] = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in r2.last_stats.items()}
         um = r2.last_stats.get("unpack_ms", 0.0)
@@ -444,7 +461,7 @@ def ours(args):
             e2e["unpack_roofline"] = {"kernel": "unpack_kernel", "bound": "hbm", "achieved": round(ub / (um / 1e3) / 1e9, 1),
                                       "peak": hbm_peak, "unit": "GB/s", "frac": round(ub / (um / 1e3) / 1e9 / hbm_peak, 3),
                                       "alg_bytes": int(ub), "kernel_ms": round(um, 3)}
-        del rs, r, r2
+        del rs, r, r2, r3
         eng_io.shutdown()
     else:
         eng.shutdown()

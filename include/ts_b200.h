@@ -313,7 +313,12 @@ typedef struct ts_restore_stats {
   double read_s, verify_s, h2d_unpack_s, total_s;
   float unpack_ms, h2d_ms;
   uint32_t kernel_launches;
+  uint32_t _pad;
+  uint64_t direct_bytes; /* fixed-region bytes copied H2D straight from page-locked files (no pread) */
 } ts_restore_stats;
+/* 1 (default): files page-locked by this process (file_dma rotation) are read
+ * by the copy engines from their page cache; 0: always pread into pinned memory. */
+ts_status ts_restore_set_file_cache(ts_restore* r, int use);
 ts_status ts_restore_rank(ts_restore* r, int index, const ts_object_desc* dst, size_t n,
                           int device, void* stream, ts_restore_stats* stats);
 ts_status ts_restore_structured(ts_restore* r, int index, uint64_t object_id, ts_value** out);

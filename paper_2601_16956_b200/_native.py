@@ -132,7 +132,8 @@ class RestoreObject(C.Structure):
 class RestoreStats(C.Structure):
     _fields_ = [("bytes", C.c_uint64), ("read_s", C.c_double), ("verify_s", C.c_double),
                 ("h2d_unpack_s", C.c_double), ("total_s", C.c_double), ("unpack_ms", C.c_float),
-                ("h2d_ms", C.c_float), ("kernel_launches", C.c_uint32)]
+                ("h2d_ms", C.c_float), ("kernel_launches", C.c_uint32), ("_pad", C.c_uint32),
+                ("direct_bytes", C.c_uint64)]
 
 
 class VerifyIssue(C.Structure):
@@ -190,6 +191,7 @@ _sig("ts_engine_destroy", i32, P)
 _sig("ts_retire_checkpoint", i32, C.c_char_p, C.c_char_p)
 _sig("ts_engine_set_spare_dir", i32, P, C.c_char_p)
 _sig("ts_engine_numa_node", i32, P)
+_sig("ts_restore_set_file_cache", i32, P, i32)
 _sig("ts_file_cache_bytes", C.c_uint64)
 _sig("ts_file_cache_release_all", i32, C.POINTER(C.c_uint64))
 _sig("ts_session_create", i32, C.c_char_p, u64, u64, C.POINTER(ManifestEcho), i32, i32, C.POINTER(P))

@@ -85,7 +85,7 @@ uint8_t* file_registry::claim(int fd, uint64_t len, file_key* key) {
   auto it = m_.find(s.key);
   if (it == m_.end()) return nullptr;
   entry& e = it->second;
-  if (e.in_use) return nullptr;
+  if (e.in_use || e.readers > 0) return nullptr;  // (a restore is reading it: leave it alone)
   if (e.pending) {
     FTRACE("claim ino=%llu pending", (unsigned long long)s.key.ino);
     // Still being registered: not usable now. Truncation to >= len keeps the
@@ -104,6 +104,27 @@ uint8_t* file_registry::claim(int fd, uint64_t len, file_key* key) {
   FTRACE("claim ino=%llu ok len=%llu", (unsigned long long)s.key.ino, (unsigned long long)len);
   e.in_use = true;
   return e.map;
+}
+
+const uint8_t* file_registry::acquire_read(int fd, uint64_t len, file_key* key) {
+  file_stat s;
+  if (!stat_fd(fd, &s)) return nullptr;
+  *key = s.key;
+  std::lock_guard<std::mutex> g(mu_);
+  auto it = m_.find(s.key);
+  if (it == m_.end()) return nullptr;
+  entry& e = it->second;
+  if (e.pending || e.in_use || e.len != len || e.size != s.size || e.mtime_ns != s.mtime_ns ||
+      !pages_present(e.map, e.maplen))
+    return nullptr;
+  e.readers += 1;
+  return e.map;
+}
+
+void file_registry::release_read(const file_key& key) {
+  std::lock_guard<std::mutex> g(mu_);
+  auto it = m_.find(key);
+  if (it != m_.end() && it->second.readers > 0) it->second.readers -= 1;
 }
 
 void file_registry::release(const file_key& key, int fd, bool ok) {
@@ -129,7 +150,7 @@ bool file_registry::want_register(int fd, uint64_t len, file_key* key) {
   auto it = m_.find(s.key);
   if (it != m_.end()) {
     entry& e = it->second;
-    if (e.in_use) return false;
+    if (e.in_use || e.readers > 0) return false;
     if (e.pending) {
       if (e.len != len) e.stale = true;
       else e.size = s.size, e.mtime_ns = s.mtime_ns;  // rewritten by us while being locked
@@ -208,7 +229,7 @@ void file_registry::sweep() {
   for (auto it = m_.begin(); it != m_.end();) {
     auto cur = it++;
     const entry& e = cur->second;
-    if (e.pending || e.in_use) continue;
+    if (e.pending || e.in_use || e.readers > 0) continue;
     file_stat s;
     if (!stat_fd(e.fd, &s) || s.nlink == 0) drop_locked(cur);
   }
@@ -219,7 +240,7 @@ uint64_t file_registry::release_all() {
   uint64_t bytes = 0;
   for (auto it = m_.begin(); it != m_.end();) {
     auto cur = it++;
-    if (cur->second.pending || cur->second.in_use) continue;
+    if (cur->second.pending || cur->second.in_use || cur->second.readers > 0) continue;
     bytes += cur->second.maplen;
     drop_locked(cur);
   }

@@ -57,6 +57,12 @@ class file_registry {
   bool want_register(int fd, uint64_t len, file_key* key);
   // mmap + cudaHostRegister (slow: run on a worker thread).
   void register_file(const file_key& key, int device);
+  // Restore side: the locked mapping of a file whose registration covers
+  // exactly [0, len) and is intact (same checks as claim), pinned against
+  // claims and drops until release_read(); nullptr otherwise. The copy engines
+  // then read the fixed region straight from the page cache.
+  const uint8_t* acquire_read(int fd, uint64_t len, file_key* key);
+  void release_read(const file_key& key);
   // Drop registrations of files that no longer have a name.
   void sweep();
   // Drop every idle registration; returns bytes released.
@@ -69,6 +75,7 @@ class file_registry {
     uint8_t* map = nullptr;
     uint64_t len = 0, maplen = 0;
     bool pending = false, stale = false, in_use = false;
+    int readers = 0;
     int64_t size = -1, mtime_ns = -1;
   };
   void drop_locked(std::map<file_key, entry>::iterator it);

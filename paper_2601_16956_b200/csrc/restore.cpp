@@ -226,6 +226,35 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
     fds[k].fd = ::open(rc.files[k].path.c_str(), O_RDONLY);
     if (fds[k].fd < 0) fail(TS_ERR_MISSING_FILE, "cannot open " + rc.files[k].path);
   }
+  // Page-locked files (registered by this process's engines): H2D straight
+  // from the page cache, no pread. Pinned against claims/drops until the end.
+  struct reg_reads {
+    std::vector<const uint8_t*> map;
+    std::vector<file_key> key;
+    ~reg_reads() {
+      for (size_t k = 0; k < map.size(); ++k)
+        if (map[k]) file_registry::get().release_read(key[k]);
+    }
+  } regs;
+  regs.map.assign(rc.files.size(), nullptr);
+  regs.key.resize(rc.files.size());
+  uint64_t direct_bytes = 0;
+  if (use_file_cache)
+    for (size_t k = 0; k < rc.files.size(); ++k)
+      if (file_img[k].second > 0) {
+        regs.map[k] = file_registry::get().acquire_read(fds[k].fd, rc.files[k].region_end, &regs.key[k]);
+        if (regs.map[k]) direct_bytes += file_img[k].second;
+      }
+  // host address of image byte `pos` of a window staged at `hs` ([lo, hi))
+  auto host_src = [&](uint64_t pos, uint64_t lo, const uint8_t* hs) -> const uint8_t* {
+    size_t k = std::upper_bound(file_img.begin(), file_img.end(), pos,
+                                [](uint64_t x, const std::pair<uint64_t, uint64_t>& f) { return x < f.first; }) -
+               file_img.begin();
+    k = k ? k - 1 : 0;
+    if (regs.map[k] && pos >= file_img[k].first && pos < file_img[k].first + file_img[k].second)
+      return regs.map[k] + header_reserved + (pos - file_img[k].first);
+    return hs + (pos - lo);
+  };
 
   struct shared_state {
     std::mutex mu;
@@ -265,7 +294,9 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
   };
   // Window finished reading: host-tier pieces to their buffers, device part
   // H2D + scatter-unpack, slot freed by a stream callback.
-  auto window_read = [&](uint64_t lo, uint64_t hi, int slot) {
+  // `direct`: the window has bytes in page-locked files (copied from there,
+  // file segment by file segment, instead of from the pinned slot).
+  auto window_read = [&](uint64_t lo, uint64_t hi, int slot, bool direct) {
     uint8_t* hs = hring + static_cast<uint64_t>(slot) * W;
     auto pit = std::lower_bound(pieces.begin(), pieces.end(), lo,
                                 [](const rpiece& p, uint64_t x) { return p.pos + p.len <= x; });
@@ -275,11 +306,21 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
       const uint64_t a = std::max(lo, pit->pos), b = std::min(hi, pit->pos + pit->len);
       if (b > a)
         std::memcpy(static_cast<uint8_t*>(const_cast<void*>(o.d->data)) + pit->obj_off + (a - pit->pos),
-                    hs + (a - lo), b - a);
+                    direct ? host_src(a, lo, hs) : hs + (a - lo), b - a);
     }
     std::lock_guard<std::mutex> g(cuda_mu);
     uint8_t* ds = dring + static_cast<uint64_t>(slot) * W;
-    cuda_check(cudaMemcpyAsync(ds, hs, hi - lo, cudaMemcpyHostToDevice, st), "H2D window");
+    if (!direct) {
+      cuda_check(cudaMemcpyAsync(ds, hs, hi - lo, cudaMemcpyHostToDevice, st), "H2D window");
+    } else {
+      for (size_t k = 0; k < rc.files.size(); ++k) {
+        const uint64_t a = std::max(lo, file_img[k].first);
+        const uint64_t b = std::min(hi, file_img[k].first + file_img[k].second);
+        if (b > a)
+          cuda_check(cudaMemcpyAsync(ds + (a - lo), host_src(a, lo, hs), b - a, cudaMemcpyHostToDevice, st),
+                     "H2D window");
+      }
+    }
     auto uit = std::lower_bound(usegs.begin(), usegs.end(), lo,
                                 [](const dev::useg& u, uint64_t x) { return u.pos + u.len <= x; });
     if (uit != usegs.end() && uit->pos < hi) {
@@ -323,18 +364,30 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
       };
       auto ws = std::make_shared<wstate>();
       std::vector<std::tuple<size_t, uint64_t, uint64_t>> reads;
+      bool direct = false;
       for (size_t k = 0; k < rc.files.size(); ++k) {
         const uint64_t a = std::max(lo, file_img[k].first);
         const uint64_t b = std::min(hi, file_img[k].first + file_img[k].second);
+        if (b > a && regs.map[k]) {
+          direct = true;  // no pread: the copy engine reads the locked pages
+          continue;
+        }
         for (uint64_t x = a; x < b; x += (16ull << 20)) reads.emplace_back(k, x, std::min<uint64_t>(b, x + (16ull << 20)));
       }
       if (reads.empty()) {
-        window_read(lo, hi, slot);
+        try {
+          window_read(lo, hi, slot, direct);
+        } catch (const error& e) {
+          set_err(e);
+          std::lock_guard<std::mutex> g(S.mu);
+          S.slot_busy[slot] = 0;
+          S.cv.notify_all();
+        }
         continue;
       }
       ws->left = static_cast<int>(reads.size());
       for (auto [k, x, y] : reads) {
-        pool.submit([&, ws, k, x, y, lo, hi, slot, hs] {
+        pool.submit([&, ws, k, x, y, lo, hi, slot, hs, direct] {
           try {
             pread_all(fds[k].fd, hs + (x - lo), y - x, header_reserved + (x - file_img[k].first), rc.files[k].path);
           } catch (const error& e) {
@@ -342,7 +395,7 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
           }
           if (--ws->left == 0) {
             try {
-              window_read(lo, hi, slot);
+              window_read(lo, hi, slot, direct);
             } catch (const error& e) {
               set_err(e);
               std::lock_guard<std::mutex> g(S.mu);
@@ -466,6 +519,7 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
     stats->verify_s = (now_ns() - t_verify) * 1e-9;
     stats->h2d_unpack_s = h2d_ms * 1e-3;
     stats->h2d_ms = h2d_ms;
+    stats->direct_bytes = direct_bytes;
     stats->unpack_ms = unpack_ms;
     stats->total_s = (now_ns() - t_begin) * 1e-9;
     stats->kernel_launches = launches;

@@ -28,6 +28,9 @@ struct restore_handle {
   manifest m;
   std::string base;
   std::vector<rank_cache> ranks;
+  // Files page-locked by this process (file_dma rotation) are read by the copy
+  // engines straight from their page cache instead of pread into pinned memory.
+  bool use_file_cache = true;
 
   explicit restore_handle(const std::string& manifest_path);
   void load_rank(int index);

@@ -185,3 +185,23 @@ def test_deleted_files_are_unlocked(gpu, shm):
     out = os.path.join(shm, "after")
     checkpoint_recipe(rec, out, cfg_for("ring"))
     assert api.file_cache_bytes() == 0
+
+
+@pytest.mark.parametrize("use_cache", [True, False])
+def test_restore_from_locked_files(gpu, shm, use_cache):
+    """Restore of a checkpoint whose files this process page-locked: the copy
+    engines read them straight from the page cache (or pread when disabled);
+    bit-exact either way."""
+    rec = load("hand_mixed")
+    rotate(rec, shm, cfg_for("ring"), rounds=2)
+    man = os.path.join(shm, "c1", "MANIFEST.tlv")
+    r = api.Restorer(man, use_file_cache=use_cache)
+    direct = 0
+    for i, spec in enumerate(rec.ranks):
+        rs = r.restore_rank(i, 0)
+        direct += r.last_stats["direct_bytes"]
+        for o, so in zip(rs.objects, spec.objects):
+            o.pattern_space, o.pattern_offset = so.space, so.offset
+        rs.seed = spec.seed
+        assert api.pattern_mismatches(rs, rec.pit) == 0
+    assert (direct > 0) == use_cache
