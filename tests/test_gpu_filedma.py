@@ -205,3 +205,48 @@ def test_restore_from_locked_files(gpu, shm, use_cache):
         rs.seed = spec.seed
         assert api.pattern_mismatches(rs, rec.pit) == 0
     assert (direct > 0) == use_cache
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_rotation_parity(gpu, shm, oracle, seed):
+    """Random states and engine configs, checkpointed with rotation: each round
+    recycles the previous round's files (page-locked when the layout matches,
+    dropped when it does not) and must equal the oracle's canonical tree."""
+    import random
+
+    from test_gpu_fuzz import random_cfg, random_recipe
+
+    rng = random.Random(5000 + seed)
+    recs = [random_recipe(rng)]
+    # rounds 2-3: the same state again (same layout: direct DMA), then another
+    # random state with the same rank ids (other layout: pool path)
+    recs.append(recs[0])
+    other = random_recipe(rng)
+    other.ranks = other.ranks[:len(recs[0].ranks)]
+    for r, o in zip(recs[0].ranks, other.ranks):
+        o.rank_id = r.rank_id
+    recs.append(other)
+    cfg = random_cfg(rng)
+    spare = os.path.join(shm, "spare")
+    prev = None
+    for k, rec in enumerate(recs):
+        if prev:
+            api.retire_checkpoint(prev, spare)
+        out = os.path.join(shm, f"c{k}")
+        session = api.CheckpointSession(out, rec.ckpt_id, rec.iteration, rec.manifest_echo(), n_ranks=len(rec.ranks))
+        states = [api.materialize_payloads(r, 0, rec.pit) for r in rec.ranks]
+        engines = [api.CheckpointEngine(cfg, r.rank_id, 0) for r in rec.ranks]
+        for e in engines:
+            e.set_spare_dir(spare)
+        tickets = [e.issue_checkpoint(session, s, rec.iteration) for e, s in zip(engines, states)]
+        for t in tickets:
+            t.wait_persisted()
+        session.wait_complete(120)
+        for e in engines:
+            e.shutdown()
+        ref = os.path.join(shm, f"ref{k}")
+        orec = oracle.load_recipe_text(rec.to_text())
+        oracle.write_checkpoint(orec, ref, ser_chunk=min(cfg.serialized_chunk_bytes, cfg.staging_capacity_bytes))
+        assert read_tree(out) == read_tree(ref), (seed, k, cfg)
+        shutil.rmtree(ref)
+        prev = out
