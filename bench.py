@@ -263,7 +263,11 @@ def ours(args):
     # creation), else a bounded pool with back-pressure (staging.cpp semantics)
     local_ws = int(os.environ.get("LOCAL_WORLD_SIZE", str(ws)))
     avail = host_mem_avail()
-    pool_cap = int(args.pool_gb * (1 << 30)) if args.pool_gb else 64 << 30
+    # Pinned pool: windows are released as they land (device checksums) or
+    # once flushed / hashed; recycled files take the D2H directly (file_dma),
+    # so a few GiB keep the copy engines busy (8 ranks x 4 GiB per node, not
+    # 8 x the shard).
+    pool_cap = int(args.pool_gb * (1 << 30)) if args.pool_gb else 4 << 30
     if avail:  # every rank of this node pins its pool: stay well inside host RAM
         pool_cap = min(pool_cap, max(1 << 30, int(0.3 * avail / max(1, local_ws))))
     pool = (min(img_est + (64 << 20), pool_cap) + (2 << 20) - 1) // (2 << 20) * (2 << 20)
@@ -680,7 +684,7 @@ def main():
     ap.add_argument("--fresh-files", action="store_true",
                     help="e2e: new files every checkpoint (no rotation / recycling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--pool-gb", type=float, default=0.0, help="pinned pool cap (default: image, at most 64 GiB)")
+    ap.add_argument("--pool-gb", type=float, default=0.0, help="pinned pool cap (default 4 GiB)")
     ap.add_argument("--ring-gb", type=float, default=0.0,
                     help="HBM staging ring when no full device shadow fits (0 = auto: free HBM - 26 GiB)")
     ap.add_argument("--ring-chunk-gb", type=float, default=0.0, help="ring slot size (0 = auto)")

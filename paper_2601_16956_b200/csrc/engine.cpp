@@ -526,6 +526,7 @@ std::shared_ptr<ticket_state> engine::issue(const std::shared_ptr<session>& sp, 
   }
   std::unordered_map<uint32_t, uint32_t> fidx;
   uint64_t cursor = 0;
+  const std::string spare = spare_dir();
   for (const auto& fp : j->plan.files) {
     job::fstate fs;
     fs.fid = fp.file_id;
@@ -535,7 +536,7 @@ std::shared_ptr<ticket_state> engine::issue(const std::shared_ptr<session>& sp, 
     cursor += fp.tensor_region_end - header_reserved;
     const std::string fname = "file_" + std::to_string(fp.file_id) + ".bin";
     const std::string recycled =
-        spare_dir_.empty() ? std::string() : spare_dir_ + "/" + rank_dir_name(rank.rank_id) + "_" + fname;
+        spare.empty() ? std::string() : spare + "/" + rank_dir_name(rank.rank_id) + "_" + fname;
     // Every opened file passes through the registry before it is truncated
     // (locked pages must never be dropped); a valid registration of exactly
     // [0, tre) makes the file's D2H windows land in its pages.
@@ -1539,7 +1540,7 @@ void engine::file_progress(const std::shared_ptr<job>& j, size_t fi) {
     if (f.claimed && !f.released) {
       reg.release(f.key, f.w->fd(), true);
       f.released = true;
-    } else if (cfg_.file_dma && !spare_dir_.empty() && f.tre > header_reserved) {
+    } else if (cfg_.file_dma && !spare_dir().empty() && f.tre > header_reserved) {
       file_key k;
       if (reg.want_register(f.w->fd(), f.tre, &k)) {
         const int dev = device_;

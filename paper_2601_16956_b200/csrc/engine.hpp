@@ -124,7 +124,14 @@ class engine {
   int64_t pre_update_barrier(const std::shared_ptr<ticket_state>& t, cudaStream_t opt_stream,
                              int host_block);
   void shutdown();
-  void set_spare_dir(const std::string& d) { spare_dir_ = d; }
+  void set_spare_dir(const std::string& d) {
+    std::lock_guard<std::mutex> g(mu_);
+    spare_dir_ = d;
+  }
+  std::string spare_dir() {
+    std::lock_guard<std::mutex> g(mu_);
+    return spare_dir_;
+  }
   const ts_engine_config& config() const { return cfg_; }
   int device() const { return device_; }
   int numa_node() const { return numa_.node; }
