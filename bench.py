@@ -132,14 +132,21 @@ def sample_recipe(cfg: str, rank: int, max_raw: int = 8):
     return rec
 
 
-def run_reference(args, sample_max_raw=8, steps=None, warmup=None):
+def run_reference(args, sample_max_raw=None, steps=None, warmup=None):
     """The reference CPU implementation (oracle/_ref/ts_ref_driver, built from
     /root/reference) on a bounded sample of this config, one process, its default
-    4 flush workers + 1 copier thread, files to /dev/shm."""
+    flush workers on every other host core + its 1 copier thread, files to /dev/shm."""
     drv = os.path.join(ROOT, "oracle", "_ref", "ts_ref_driver")
     if not os.path.exists(drv):
         return None
+    from paper_2601_16956_b200 import synthetic as S
+
+    if sample_max_raw is None:  # the whole rank when it is small (cfg1), else a ~3 GB sample
+        full = S.config_recipe(args.config, 0).ranks[0]
+        sample_max_raw = len(full.objects) if full.raw_bytes <= (4 << 30) else 8
     rec = sample_recipe(args.config, 0, sample_max_raw)
+    whole = len([o for o in rec.ranks[0].objects if o.kind == 0]) == len(
+        [o for o in S.config_recipe(args.config, 0).ranks[0].objects if o.kind == 0])
     sample_bytes = rec.ranks[0].raw_bytes
     tmp = tempfile.mkdtemp(dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
     try:
@@ -147,7 +154,8 @@ def run_reference(args, sample_max_raw=8, steps=None, warmup=None):
         with open(rp, "w") as f:
             f.write(rec.to_text())
         cap = 1 << (max(sample_bytes, 256 << 20) - 1).bit_length()
-        cmd = [drv, "bench", rp, os.path.join(tmp, "ckpt"), "--workers", "4", "--cache", str(cap),
+        workers = max(4, (os.cpu_count() or 8) - 1)  # all the host threads it can use
+        cmd = [drv, "bench", rp, os.path.join(tmp, "ckpt"), "--workers", str(workers), "--cache", str(cap),
                "--reps", str(steps if steps is not None else 1), "--warmup",
                str(warmup if warmup is not None else 0)]
         out = subprocess.run(cmd, capture_output=True, text=True, check=True).stdout
@@ -162,7 +170,8 @@ def run_reference(args, sample_max_raw=8, steps=None, warmup=None):
             "bytes_per_step": timed[0]["bytes"], "snapshot_s": [r["snapshot_s"] for r in timed],
             "issue_ms": [1e3 * r["issue_s"] for r in timed],
             "sample": f"{args.config} rank 0: first {sample_max_raw} raw objects + metadata "
-                      f"({timed[0]['bytes'] / 1e9:.2f} GB), lazy, 4 flush workers, files on /dev/shm"}
+                      f"({timed[0]['bytes'] / 1e9:.2f} GB), lazy, {workers} flush workers + 1 copier, files on /dev/shm",
+            "cores": workers + 1, "whole": whole}
 
 
 def reference_arm(args):
@@ -177,9 +186,10 @@ def reference_arm(args):
             "unit": "GB/s", "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
             "ms_per_step": round(1e3 * statistics.mean(r["snapshot_s"]), 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": args.config + " (bounded CPU sample)", "sample": r["sample"]},
+            "config": {"workload": args.config + (" (whole rank)" if r["whole"] else " (bounded CPU sample)"),
+                       "sample": r["sample"]},
             "persist_gbps": round(r["persist_gbps"], 4), "blocked_ms": round(statistics.mean(r["issue_ms"]), 3),
-            "cpu_baseline": {"value": round(r["value"], 4), "unit": "GB/s", "cores": 5, "kind": "reference",
+            "cpu_baseline": {"value": round(r["value"], 4), "unit": "GB/s", "cores": r["cores"], "kind": "reference",
                              "sample": r["sample"]},
             "e2e": {"value": round(r["value"], 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -486,7 +496,7 @@ def ours(args):
     if rank == 0 and not args.no_cpu_baseline:
         r = run_reference(args)
         if r:
-            cpu = {"value": round(r["value"], 4), "unit": "GB/s", "cores": 5, "kind": "reference",
+            cpu = {"value": round(r["value"], 4), "unit": "GB/s", "cores": r["cores"], "kind": "reference",
                    "sample": r["sample"]}
     clocks = clk.summary()
     if rank == 0:
