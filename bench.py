@@ -563,6 +563,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
     comp = torch.cuda.current_stream()
     res = {"off": ([], []), "lazy": ([], [])}
     host_ck = []
+    issue_cpp, issue_py = [], []  # issue time inside the engine vs the whole Python call
     clk = {"off": [], "lazy": []}
     fb_gpu = {"off": [], "lazy": []}  # CUDA-event time of fwd+bwd on the compute stream
     phases = {"off": [], "lazy": []}  # host wall per step phase
@@ -627,7 +628,10 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
                 if files:
                     ckpts.append((d, sess, pending))
                 if k > 0:
-                    host_ck.append(pending.stats()["host_checksum_bytes"] / max(1, spec.raw_bytes))
+                    st_k = pending.stats()
+                    host_ck.append(st_k["host_checksum_bytes"] / max(1, spec.raw_bytes))
+                    issue_cpp.append(st_k["issue_block_ns"] / 1e6)
+                    issue_py.append(1e3 * ib)
             p_iss = time.perf_counter()
             comp.synchronize()
             if k > 0:
@@ -657,6 +661,8 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
             "blocked_ms_per_ckpt": round(res["lazy"][1], 3),
             "host_checksum_frac": round(statistics.mean(host_ck), 3) if host_ck else None,
             "rotation_wait_ms": round(1e3 * statistics.mean(rot_wait), 2) if rot_wait else None,
+            "issue_ms": {"engine": round(statistics.mean(issue_cpp), 3) if issue_cpp else None,
+                         "python_call": round(statistics.mean(issue_py), 3) if issue_py else None},
             "fwd_bwd_gpu_ms": {m: round(statistics.mean(v), 1) for m, v in fb_gpu.items() if v},
             "phase_ms": {m: dict(zip(["fwd_bwd", "barrier", "update_launch", "issue", "final_sync"],
                                      [round(1e3 * statistics.mean(x), 2) for x in zip(*v)]))
