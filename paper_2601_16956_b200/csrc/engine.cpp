@@ -19,6 +19,17 @@ void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(TS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  // (the end event may trail the work that was observed complete by a few
+  // commands on its stream)
+  if (cudaEventSynchronize(b) != cudaSuccess || cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+    cudaGetLastError();  // clear: unrecorded events are not an error here
+    return 0;
+  }
+  return ms;
+}
+
 namespace {
 const bool g_trace = std::getenv("TS_TRACE") != nullptr;
 #define TRACE(...)                                                                     \
@@ -1482,14 +1493,15 @@ void engine::check_snapshot(const std::shared_ptr<job>& j) {
         TRACE("snapshot rank=%d", j->rank_id);
         j->t->snapshot = true;
         j->t->t_snapshot = now_ns() - j->t->t_issue;
-        cudaEventElapsedTime(&j->t->d2h_ms, j->t->ev_d2h_first, j->t->ev_d2h_last);
+        // (events of an empty image were never recorded; a failed query must
+        // not leave a stale per-thread error for a later cudaGetLastError)
+        j->t->d2h_ms = j->img > 0 ? elapsed_ms(j->t->ev_d2h_first, j->t->ev_d2h_last) : 0.f;
         if (!j->pack_events.empty()) {  // RING: sum of the pack kernels alone
-          float sum = 0, ms = 0;
-          for (auto& pe : j->pack_events)
-            if (cudaEventElapsedTime(&ms, pe.first, pe.second) == cudaSuccess) sum += ms;
+          float sum = 0;
+          for (auto& pe : j->pack_events) sum += elapsed_ms(pe.first, pe.second);
           j->t->pack_ms = sum;
         } else {
-          cudaEventElapsedTime(&j->t->pack_ms, j->t->ev_pack0, j->t->ev_capture);
+          j->t->pack_ms = elapsed_ms(j->t->ev_pack0, j->t->ev_capture);
         }
         if (j->t->t_captured < 0) j->t->t_captured = j->t->t_snapshot;
       }

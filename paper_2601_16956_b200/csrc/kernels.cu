@@ -49,8 +49,7 @@ __device__ __forceinline__ uint4 funnel16(uint4 A, uint4 B, uint32_t sh) {
 
 // One warp copies n bytes s -> d (s == nullptr: zero fill). Any alignment:
 // stores are always 16-B aligned; a misaligned source is realigned with two
-// aligned loads and a funnel shift (never touching bytes outside the aligned
-// 16-B blocks that hold source bytes).
+// aligned loads and a funnel shift (every access stays inside the source).
 __device__ __forceinline__ void warp_copy(uint8_t* d, const uint8_t* s, uint64_t n, uint32_t lane) {
   uint32_t head = static_cast<uint32_t>((16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15);
   if (head > n) head = static_cast<uint32_t>(n);
@@ -78,13 +77,28 @@ __device__ __forceinline__ void warp_copy(uint8_t* d, const uint8_t* s, uint64_t
   } else {
     const uint32_t sh = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(s) & 15);
     const uint4* sa = reinterpret_cast<const uint4*>(s - sh);
-    for (; i + 32 < nv; i += 64) {
+    // The last output vector's second block sa[nv] holds needed bytes but may
+    // extend past the end of the source object (never past its aligned 16-B
+    // block, so never across a page): when it would, that vector is assembled
+    // from byte loads, keeping every access inside the object.
+    const uint64_t rem_src = n & 15;
+    const uint64_t nfast = (16 - sh <= rem_src) ? nv : (nv ? nv - 1 : 0);
+    for (; i + 32 < nfast; i += 64) {
       const uint4 a0 = ld_stream(sa + i), a1 = ld_stream(sa + i + 1);
       const uint4 b0 = ld_stream(sa + i + 32), b1 = ld_stream(sa + i + 33);
       st_stream(dv + i, funnel16(a0, a1, sh));
       st_stream(dv + i + 32, funnel16(b0, b1, sh));
     }
-    for (; i < nv; i += 32) st_stream(dv + i, funnel16(ld_stream(sa + i), ld_stream(sa + i + 1), sh));
+    for (; i < nfast; i += 32) st_stream(dv + i, funnel16(ld_stream(sa + i), ld_stream(sa + i + 1), sh));
+    if (nfast < nv && i == nv - 1) {  // this lane owns the last vector
+      const uint8_t* t = s + 16 * (nv - 1);
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        w[q] = static_cast<uint32_t>(t[4 * q]) | (static_cast<uint32_t>(t[4 * q + 1]) << 8) |
+               (static_cast<uint32_t>(t[4 * q + 2]) << 16) | (static_cast<uint32_t>(t[4 * q + 3]) << 24);
+      st_stream(dv + nv - 1, make_uint4(w[0], w[1], w[2], w[3]));
+    }
   }
   const uint32_t rem = static_cast<uint32_t>(n & 15);
   if (lane < rem) d[nv * 16 + lane] = s ? s[nv * 16 + lane] : 0;

@@ -467,13 +467,9 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
     o.hashed = o.size;
   }
   (void)d_states;
-  float h2d_ms = 0;
-  cudaEventElapsedTime(&h2d_ms, ev_a, ev_b);
+  const float h2d_ms = elapsed_ms(ev_a, ev_b);
   float unpack_ms = 0;
-  for (auto& ue : unpack_ev) {
-    float ms = 0;
-    if (cudaEventElapsedTime(&ms, ue.first, ue.second) == cudaSuccess) unpack_ms += ms;
-  }
+  for (auto& ue : unpack_ev) unpack_ms += elapsed_ms(ue.first, ue.second);
   cudaEventDestroy(ev_a);
   cudaEventDestroy(ev_b);
 
