@@ -617,12 +617,14 @@ std::shared_ptr<ticket_state> engine::issue(const std::shared_ptr<session>& sp, 
     double frac = cfg_.checksum_host_frac;
     double obj_cap = 1e30;
     if (frac < 0) {
-      // host hashing overlaps the D2H; it may also use the slack before the
-      // next checkpoint, never delay persist beyond it
+      // The FNV kernels overlap the D2H for free when nothing else runs on
+      // the GPU; host workers are worth it only for the slack before the next
+      // checkpoint (a training loop). A closed loop (caller waits for persist,
+      // no slack) keeps everything on the GPU, so host-held pool windows can
+      // never throttle the D2H. One host chain must finish within D2H + slack.
       const double d2h_s = static_cast<double>(j->img) / 50e9;
-      const double budget_s = d2h_s + slack_s_;
-      frac = dev_bytes ? std::min(1.0, 0.8 * host_rate_ * budget_s / static_cast<double>(dev_bytes)) : 0.0;
-      obj_cap = 0.8 * chain_rate_ * budget_s;
+      frac = dev_bytes ? std::min(1.0, 0.8 * host_rate_ * slack_s_ / static_cast<double>(dev_bytes)) : 0.0;
+      obj_cap = 0.8 * chain_rate_ * (d2h_s + slack_s_);
     }
     uint64_t seen = 0, host = 0;
     for (size_t k = 0; k < j->raws.size(); ++k) {
