@@ -625,6 +625,12 @@ std::shared_ptr<ticket_state> engine::issue(const std::shared_ptr<session>& sp, 
       const double d2h_s = static_cast<double>(j->img) / 50e9;
       frac = dev_bytes ? std::min(1.0, 0.8 * host_rate_ * slack_s_ / static_cast<double>(dev_bytes)) : 0.0;
       obj_cap = 0.8 * chain_rate_ * (d2h_s + slack_s_);
+      // Host-hashed windows that land in the pinned pool hold it until hashed:
+      // only when the pool takes all of them can hashing not throttle the D2H.
+      uint64_t pool_bytes = 0;
+      for (const auto& f : j->files)
+        if (!(j->io && f.dma)) pool_bytes += f.tre - header_reserved;
+      if (pool_bytes > pool_->capacity()) frac = 0.0;
     }
     uint64_t seen = 0, host = 0;
     for (size_t k = 0; k < j->raws.size(); ++k) {
