@@ -162,3 +162,20 @@ def test_session_manifest_matches_oracle(native, oracle, tmp_path):
         with open(os.path.join(d, "MANIFEST.tlv"), "rb") as f, \
                 open(os.path.join(GOLDEN, "trees", name, "MANIFEST.tlv"), "rb") as g:
             assert f.read() == g.read(), name
+
+
+def test_capi_caller_compiles_against_header(native, tmp_path):
+    """include/ts_b200.h is enough to build a C++ caller (tests/capi/capi_checkpoint.cpp)
+    that links the library; run on a GPU by tests/test_gpu_capi.py."""
+    import subprocess
+
+    from paper_2601_16956_b200 import build as B
+
+    lib = B.build()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "capi_checkpoint")
+    subprocess.run(["g++", "-O2", "-std=c++17", "-Wall", "-Werror", "-I", os.path.join(root, "include"),
+                    "-I", "/usr/local/cuda/include", os.path.join(root, "tests", "capi", "capi_checkpoint.cpp"),
+                    "-o", exe, "-L", os.path.dirname(lib), "-lts_b200", "-L", "/usr/local/cuda/lib64",
+                    "-lcudart_static", "-ldl", "-lrt", "-lpthread"], check=True)
+    assert os.path.getsize(exe) > 0
