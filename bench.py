@@ -493,7 +493,7 @@ def ours(args):
         blocked = training_phase(args, api, state, spec, cfg, local_dev, dev, it)
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:  # (N=1 only)
         r = run_reference(args)
         if r:
             cpu = {"value": round(r["value"], 4), "unit": "GB/s", "cores": r["cores"], "kind": "reference",
