@@ -157,7 +157,7 @@ def run_reference(args, sample_max_raw=None, steps=None, warmup=None):
         workers = max(4, (os.cpu_count() or 8) - 1)  # all the host threads it can use
         cmd = [drv, "bench", rp, os.path.join(tmp, "ckpt"), "--workers", str(workers), "--cache", str(cap),
                "--reps", str(steps if steps is not None else 1), "--warmup",
-               str(warmup if warmup is not None else 0)]
+               str(warmup if warmup is not None else 0), "--restore"]
         out = subprocess.run(cmd, capture_output=True, text=True, check=True).stdout
         rows = [json.loads(l) for l in out.splitlines() if l.startswith("{")]
     finally:
@@ -166,7 +166,9 @@ def run_reference(args, sample_max_raw=None, steps=None, warmup=None):
     snap = sum(r["snapshot_s"] for r in timed)
     pers = sum(r["persist_s"] for r in timed)
     b = sum(r["bytes"] for r in timed)
+    rest = [r["restore_s"] for r in timed if r.get("restore_s", -1) > 0]
     return {"value": b / snap / 1e9, "persist_gbps": b / pers / 1e9, "steps": len(timed),
+            "restore_gbps": round(timed[0]["bytes"] * len(rest) / sum(rest) / 1e9, 4) if rest else None,
             "bytes_per_step": timed[0]["bytes"], "snapshot_s": [r["snapshot_s"] for r in timed],
             "issue_ms": [1e3 * r["issue_s"] for r in timed],
             "sample": f"{args.config} rank 0: first {sample_max_raw} raw objects + metadata "
@@ -188,7 +190,8 @@ def reference_arm(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": args.config + (" (whole rank)" if r["whole"] else " (bounded CPU sample)"),
                        "sample": r["sample"]},
-            "persist_gbps": round(r["persist_gbps"], 4), "blocked_ms": round(statistics.mean(r["issue_ms"]), 3),
+            "persist_gbps": round(r["persist_gbps"], 4), "restore_gbps": r["restore_gbps"],
+            "blocked_ms": round(statistics.mean(r["issue_ms"]), 3),
             "cpu_baseline": {"value": round(r["value"], 4), "unit": "GB/s", "cores": r["cores"], "kind": "reference",
                              "sample": r["sample"]},
             "e2e": {"value": round(r["value"], 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
@@ -497,6 +500,7 @@ def ours(args):
         r = run_reference(args)
         if r:
             cpu = {"value": round(r["value"], 4), "unit": "GB/s", "cores": r["cores"], "kind": "reference",
+                   "restore_gbps": r["restore_gbps"],
                    "sample": r["sample"]}
     clocks = clk.summary()
     if rank == 0:
