@@ -267,6 +267,17 @@ def ours(args):
     spec = rec.ranks[0]
     state = api.materialize_payloads(spec, local_dev, 0)
     raw = spec.raw_bytes
+    # D2H load balancing: a rank above the mean shard hands part
+    # of its image to the copy engines of the GPUs below it (NVLink read, their
+    # PCIe links). One allgather of shard sizes at setup; nothing per step.
+    helpers, share = (), 0.0
+    if ws > 1 and args.balance:
+        sizes = [None] * ws
+        dist.all_gather_object(sizes, (rank, local_dev, raw))
+        mean = sum(s[2] for s in sizes) / ws
+        if raw > 1.05 * mean:
+            helpers = tuple(sorted({d for _, d, r in sizes if r < mean}))
+            share = (raw - mean) / raw if helpers else 0.0
     img_est = raw + 4096 * (len(spec.objects) + 4)
     free, _ = torch.cuda.mem_get_info(local_dev)
     shadow = img_est + (256 << 20) <= free - (24 << 30)  # keep room for the GEMM load
@@ -290,7 +301,7 @@ def ours(args):
                            checksum_on_gpu=not args.host_checksum, pack_kernel=args.pack_kernel,
                            checksum_priority=args.ck_priority, pack_priority=args.pack_priority,
                            checksum_host_frac=args.ck_host_frac, ring_chunk_bytes=int(args.ring_chunk_gb * (1 << 30)),
-                           worker_nice=args.worker_nice)
+                           worker_nice=args.worker_nice, helper_devices=helpers, helper_share=share)
     eng = api.CheckpointEngine(cfg, spec.rank_id, local_dev)
     numa_node = eng.numa_node
     full = getattr(rec, "full_layout", None)
@@ -516,6 +527,7 @@ def ours(args):
                        "priorities": {"pack": args.pack_priority, "checksums": args.ck_priority},
                        "checksum_host_frac": "auto" if args.ck_host_frac < 0 else args.ck_host_frac,
                        "numa_node": numa_node, "l2": "inputs > L2 (126 MB)",
+                       "d2h_helpers": {"devices": list(helpers), "share": round(share, 3)},
                        "step": "update(pattern kernel) + issue + snapshot + checksums (no files)"},
             "per_gpu_gbps": round(value / ws, 3),
             "snapshot_ms_mean": round(statistics.mean(snap_ms), 2),
@@ -709,6 +721,8 @@ def main():
                     help="HBM staging ring when no full device shadow fits (0 = auto: free HBM - 26 GiB)")
     ap.add_argument("--ring-chunk-gb", type=float, default=0.0, help="ring slot size (0 = auto)")
     ap.add_argument("--worker-nice", type=int, default=10, help="nice increment of engine worker threads")
+    ap.add_argument("--no-balance", dest="balance", action="store_false",
+                    help="N>1: no D2H load balancing onto helper GPUs")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)

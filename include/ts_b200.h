@@ -197,6 +197,13 @@ typedef struct ts_engine_config {
                                        NUMA node (multi-socket hosts; no-op on one node) */
   int32_t worker_nice;              /* nice increment of the worker threads (default 10: background
                                        to the training process's launching thread); 0 = none */
+  uint32_t helper_mask;             /* RING: devices (bit i = device i) whose copy engines may carry
+                                       part of this rank's D2H, reading the staged image over NVLink
+                                       (peer access) into host memory through their own PCIe links:
+                                       load balancing for ranks holding more than their share
+                                       (cfg2's dp-0 rank). 0 (default): none */
+  uint32_t _pad4;
+  double helper_share;              /* fraction of the image the helpers carry, spread evenly */
 } ts_engine_config;
 
 void ts_engine_config_default(ts_engine_config* cfg);
@@ -278,6 +285,7 @@ typedef struct ts_ticket_stats {
   int32_t snapshot_done, persisted_done, failed;
   uint64_t file_dma_bytes; /* fixed-region bytes the copy engines wrote straight into file pages */
   uint64_t host_checksum_bytes; /* device-tier bytes hashed by host workers (rest: FNV kernels) */
+  uint64_t helper_bytes;        /* image bytes D2H'd by helper GPUs (helper_mask) */
 } ts_ticket_stats;
 ts_status ts_ticket_stats_get(ts_ticket* t, ts_ticket_stats* out);
 /* Per-object checksum accumulated at staging (transfer.cpp:163-166) */

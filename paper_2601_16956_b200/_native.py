@@ -103,7 +103,8 @@ class EngineConfigC(C.Structure):
                 ("checksum_on_gpu", C.c_int32), ("flush_mmap", C.c_int32), ("pack_kernel", C.c_int32),
                 ("bulk_min_bytes", C.c_uint64), ("file_dma", C.c_int32), ("checksum_priority", C.c_int32),
                 ("_pad2", C.c_int32), ("checksum_host_frac", C.c_double), ("ring_chunk_bytes", C.c_uint64),
-                ("numa_bind", C.c_int32), ("worker_nice", C.c_int32)]
+                ("numa_bind", C.c_int32), ("worker_nice", C.c_int32),
+                ("helper_mask", C.c_uint32), ("_pad4", C.c_uint32), ("helper_share", C.c_double)]
 
 
 class ManifestEcho(C.Structure):
@@ -120,7 +121,7 @@ class TicketStats(C.Structure):
                 ("pack_ms", C.c_float), ("d2h_ms", C.c_float), ("kernel_launches", C.c_uint32),
                 ("copies", C.c_uint32), ("snapshot_done", C.c_int32), ("persisted_done", C.c_int32),
                 ("failed", C.c_int32), ("file_dma_bytes", C.c_uint64),
-                ("host_checksum_bytes", C.c_uint64)]
+                ("host_checksum_bytes", C.c_uint64), ("helper_bytes", C.c_uint64)]
 
 
 class RestoreObject(C.Structure):

@@ -338,6 +338,8 @@ class EngineConfig:
     ring_chunk_bytes: int = 0  # RING slot size without a full shadow (0 = auto: ring/6, <= 8 GiB)
     numa_bind: bool = True  # engine threads + pinned pool on the GPU's NUMA node (multi-socket hosts)
     worker_nice: int = 10  # nice increment of the background worker threads (0 = none)
+    helper_devices: tuple = ()  # RING: GPUs whose copy engines carry part of this rank's D2H (NVLink read)
+    helper_share: float = 0.0  # fraction of the image they carry
 
     def to_c(self) -> N.EngineConfigC:
         c = N.EngineConfigC()
@@ -368,6 +370,8 @@ class EngineConfig:
         c.ring_chunk_bytes = int(self.ring_chunk_bytes)
         c.numa_bind = int(self.numa_bind)
         c.worker_nice = int(self.worker_nice)
+        c.helper_mask = sum(1 << int(d) for d in self.helper_devices)
+        c.helper_share = float(self.helper_share)
         return c
 
 

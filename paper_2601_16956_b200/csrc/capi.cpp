@@ -203,6 +203,8 @@ void ts_engine_config_default(ts_engine_config* c) {
   c->ring_chunk_bytes = 0;
   c->numa_bind = 1;
   c->worker_nice = 10;
+  c->helper_mask = 0;
+  c->helper_share = 0.0;
 }
 
 ts_status ts_engine_create(const ts_engine_config* cfg, int rank_id, int device, ts_engine** out) {
@@ -358,6 +360,7 @@ ts_status ts_ticket_stats_get(ts_ticket* t, ts_ticket_stats* o) {
     o->failed = s.failed;
     o->file_dma_bytes = s.file_dma_bytes;
     o->host_checksum_bytes = s.host_checksum_bytes;
+    o->helper_bytes = s.helper_bytes;
   });
 }
 

@@ -250,6 +250,7 @@ struct job {
     pinned_pool::region r;
     uint8_t* host = nullptr;  // landing address: the pool region, or the file pages (dma)
     bool dma = false;
+    int helper = -1;  // index into engine::helpers_ when a helper GPU copies this window
     cudaEvent_t ev = nullptr;
     int refs = 0;
     uint32_t wp_begin = 0, wp_end = 0, fs_begin = 0, fs_end = 0, hp_begin = 0, hp_end = 0;
@@ -374,6 +375,29 @@ engine::engine(const ts_engine_config& cfg, int rank_id, int device)
   // work: a lower CPU priority keeps the training process's kernel-launching
   // thread responsive when every core is hashing.
   const int nice_inc = cfg_.worker_nice;
+  // Helper GPUs for D2H load balancing (RING): a stream on each, with peer
+  // access to this GPU's memory (the staged image is read over NVLink).
+  for (int d = 0; d < 32; ++d) {
+    if (!(cfg_.helper_mask & (1u << d)) || d >= ndev) continue;
+    if (d != device_) {
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, d, device_);
+      if (!can) continue;
+    }
+    auto h = std::make_unique<helper_dev>();
+    h->dev = d;
+    cuda_check(cudaSetDevice(d), "cudaSetDevice(helper)");
+    if (d != device_) {
+      const cudaError_t pe = cudaDeviceEnablePeerAccess(device_, 0);
+      if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) cuda_check(pe, "peer access (helper)");
+      cudaGetLastError();
+    }
+    int hlo = 0, hhi = 0;
+    cudaDeviceGetStreamPriorityRange(&hlo, &hhi);
+    cuda_check(cudaStreamCreateWithPriority(&h->st, cudaStreamNonBlocking, hlo), "helper stream");
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    helpers_.push_back(std::move(h));
+  }
   workers_ = std::make_unique<thread_pool>(cfg_.flush_workers, [this, nice_inc] {
     numa_bind_thread(numa_);
     if (nice_inc > 0) setpriority(PRIO_PROCESS, static_cast<id_t>(syscall(SYS_gettid)), nice_inc);
@@ -392,6 +416,12 @@ engine::~engine() {
   if (ck_host_) cudaFreeHost(ck_host_);
   if (pack_stream_) cudaStreamDestroy(pack_stream_);
   if (ck_stream_) cudaStreamDestroy(ck_stream_);
+  for (auto& h : helpers_) {
+    cudaSetDevice(h->dev);
+    for (auto e : h->free_ev) cudaEventDestroy(e);
+    if (h->st) cudaStreamDestroy(h->st);
+  }
+  cudaSetDevice(device_);
   if (copy_stream_) cudaStreamDestroy(copy_stream_);
   for (auto e : ev_free_) cudaEventDestroy(e);
 }
@@ -437,6 +467,29 @@ cudaEvent_t engine::get_event() {
 void engine::put_event(cudaEvent_t e) {
   std::lock_guard<std::mutex> g(ev_mu_);
   ev_free_.push_back(e);
+}
+
+cudaEvent_t engine::helper_event(size_t k) {
+  auto& h = *helpers_[k];
+  {
+    std::lock_guard<std::mutex> g(h.mu);
+    if (!h.free_ev.empty()) {
+      auto e = h.free_ev.back();
+      h.free_ev.pop_back();
+      return e;
+    }
+  }
+  cudaEvent_t e;  // events belong to the device of the stream they are recorded on
+  cuda_check(cudaSetDevice(h.dev), "cudaSetDevice(helper)");
+  const cudaError_t ce = cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync);
+  cudaSetDevice(device_);
+  cuda_check(ce, "helper event");
+  return e;
+}
+
+void engine::put_helper_event(size_t k, cudaEvent_t e) {
+  std::lock_guard<std::mutex> g(helpers_[k]->mu);
+  helpers_[k]->free_ev.push_back(e);
 }
 
 uint8_t* engine::ensure_device_ring(uint64_t bytes) {
@@ -1022,6 +1075,8 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     const bool shadow = nslots == 1;
     j->chunk_events.assign(nchunks, nullptr);
     j->ck_events.assign(nchunks, nullptr);
+    uint64_t seen_bytes = 0, helper_done = 0;
+    size_t helper_next = 0;
     size_t w = 0;
     cuda_check(cudaEventRecord(t.ev_d2h_first, copy_stream_), "event");
     for (size_t c = 0; c < nchunks && !failed(); ++c) {
@@ -1067,12 +1122,30 @@ void engine::run_job(const std::shared_ptr<job>& j) {
         cuda_check(cudaEventRecord(ck, ck_stream_), "event");
         j->ck_events[c] = ck;
       }
+      std::vector<char> helper_used(helpers_.size(), 0);
       for (size_t q = w; q < j->wins.size() && j->wins[q].lo < chi; ++q, ++w) {
         const size_t wi = shadow ? j->worder[q] : q;
         auto& win = j->wins[wi];
         acquire(win);
-        const cudaError_t ce = cudaMemcpyAsync(win.host, slot + (win.lo - clo), win.hi - win.lo,
-                                               cudaMemcpyDeviceToHost, copy_stream_);
+        const uint64_t len = win.hi - win.lo;
+        cudaStream_t cs = copy_stream_;
+        // helper share spread evenly over the image, round robin over helpers
+        if (!helpers_.empty() && static_cast<double>(helper_done + len / 2) <
+                                     cfg_.helper_share * static_cast<double>(seen_bytes + len)) {
+          const size_t k = helper_next++ % helpers_.size();
+          put_event(win.ev);
+          win.ev = helper_event(k);
+          win.helper = static_cast<int>(k);
+          cs = helpers_[k]->st;
+          if (!helper_used[k]) {  // once per chunk: the helper copies only after the pack
+            cuda_check(cudaStreamWaitEvent(cs, packed, 0), "helper waits for the pack");
+            helper_used[k] = 1;
+          }
+          helper_done += len;
+          t.helper_bytes += len;
+        }
+        seen_bytes += len;
+        const cudaError_t ce = cudaMemcpyAsync(win.host, slot + (win.lo - clo), len, cudaMemcpyDeviceToHost, cs);
         if (ce != cudaSuccess) {
           char m[256];
           std::snprintf(m, sizeof m, "D2H window [%llu, %llu) of chunk %zu at %llu (ring %llu B, host %p dma %d)",
@@ -1081,9 +1154,16 @@ void engine::run_job(const std::shared_ptr<job>& j) {
           cuda_check(ce, m);
         }
         t.copies += 1;
-        cuda_check(cudaEventRecord(win.ev, copy_stream_), "event");
+        cuda_check(cudaEventRecord(win.ev, cs), "event");
         push_window(wi);
         if (failed()) break;
+      }
+      for (size_t k = 0; k < helpers_.size(); ++k) {  // the slot is free once the helpers' copies are done
+        if (!helper_used[k]) continue;
+        cudaEvent_t he = helper_event(k);
+        cuda_check(cudaEventRecord(he, helpers_[k]->st), "event");
+        cuda_check(cudaStreamWaitEvent(copy_stream_, he, 0), "wait helper copies");
+        put_helper_event(k, he);  // (re-recorded only after this wait was enqueued)
       }
       cudaEvent_t done;
       cuda_check(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "event");
@@ -1182,7 +1262,8 @@ void engine::completer_loop() {
     }
     auto& win = j->wins[pw.w];
     const cudaError_t e = cudaEventSynchronize(win.ev);
-    put_event(win.ev);
+    if (win.helper >= 0) put_helper_event(static_cast<size_t>(win.helper), win.ev);
+    else put_event(win.ev);
     win.ev = nullptr;
     if (e != cudaSuccess) {
       j->t->fail(TS_ERR_CUDA, std::string("staging failed: ") + cudaGetErrorString(e));

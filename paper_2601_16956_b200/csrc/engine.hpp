@@ -99,6 +99,7 @@ struct ticket_state {
   uint64_t total_bytes = 0, raw_bytes = 0, serialized_bytes = 0, image_bytes = 0;
   uint64_t file_dma_bytes = 0;  // fixed-region bytes DMA'd straight into file pages
   uint64_t host_checksum_bytes = 0;  // device-tier bytes hashed by host workers (rest: FNV kernels)
+  uint64_t helper_bytes = 0;         // image bytes D2H'd by helper GPUs' copy engines (NVLink read)
   float pack_ms = 0, d2h_ms = 0;
   uint32_t kernel_launches = 0, copies = 0;
   cudaEvent_t ev_start = nullptr, ev_capture = nullptr, ev_d2h_first = nullptr,
@@ -152,6 +153,18 @@ class engine {
   void check_snapshot(const std::shared_ptr<job>& j);
   cudaEvent_t get_event();
   void put_event(cudaEvent_t e);
+  // Helper GPUs (helper_mask): their copy engines read this GPU's staged image
+  // over NVLink (peer access) and write it to host memory through their own
+  // PCIe links — D2H load balancing for ranks holding more than their share.
+  struct helper_dev {
+    int dev = 0;
+    cudaStream_t st = nullptr;
+    std::mutex mu;
+    std::vector<cudaEvent_t> free_ev;
+  };
+  cudaEvent_t helper_event(size_t k);
+  void put_helper_event(size_t k, cudaEvent_t e);
+  std::vector<std::unique_ptr<helper_dev>> helpers_;
   uint8_t* ensure_device_ring(uint64_t bytes);
   void* ensure_seg_buffer(uint64_t bytes);
   uint8_t* ensure_fnv_buffer(uint64_t bytes);

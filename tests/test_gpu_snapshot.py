@@ -225,3 +225,22 @@ def test_checksum_split_identical(gpu, tmp_path, name, mode, frac):
         assert host == dev
     else:
         assert 0 <= host <= dev
+
+
+@pytest.mark.parametrize("share", [0.3, 1.0])
+@pytest.mark.parametrize("staging", [256 << 10, 64 << 20])  # ring of slots / full device shadow
+@pytest.mark.parametrize("name", ["hand_mixed", "odd_layout", "two_ranks", "zero3_tiny"])
+def test_helper_gpu_d2h_identical(gpu, tmp_path, name, staging, share):
+    """D2H load balancing (helper_devices): part of the windows copied by a
+    helper GPU's copy engine (here the same device through a second stream; on a
+    multi-GPU node a peer reading over NVLink) — the same bytes either way."""
+    rec = S.load_recipe(os.path.join(GOLDEN, "recipes", name + ".recipe"))
+    out = str(tmp_path / "ckpt")
+    _, _, stats, _ = checkpoint_recipe(rec, out, cfg_for("ring", device_staging_bytes=staging,
+                                                         helper_devices=(0,), helper_share=share))
+    assert read_tree(out) == read_tree(os.path.join(GOLDEN, "trees", name))
+    helper = sum(s["helper_bytes"] for s in stats)
+    image = sum(s["image_bytes"] for s in stats)
+    assert 0 < helper <= image
+    if share == 1.0:
+        assert helper == image or helper >= image - (64 << 10)  # every window (padding never moves)
