@@ -5,6 +5,7 @@
 #include <fcntl.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
+#include <sys/vfs.h>
 #include <unistd.h>
 
 #include <cstdio>
@@ -147,6 +148,14 @@ bool file_registry::want_register(int fd, uint64_t len, file_key* key) {
   if (!stat_fd(fd, &s)) return false;
   std::lock_guard<std::mutex> g(mu_);
   if (unsupported_dev_.count(s.key.dev)) return false;
+  // Only shmem pages can be pinned long term for writing (disk filesystems
+  // track dirty pages and refuse); do not even try elsewhere.
+  struct statfs fs;
+  constexpr long kTmpfsMagic = 0x01021994;
+  if (::fstatfs(fd, &fs) != 0 || static_cast<long>(fs.f_type) != kTmpfsMagic) {
+    unsupported_dev_.insert(s.key.dev);
+    return false;
+  }
   auto it = m_.find(s.key);
   if (it != m_.end()) {
     entry& e = it->second;

@@ -18,7 +18,8 @@
 //    finalize (nobody else truncated or rewrote it);
 //  * every opened file passes through claim() BEFORE it is truncated: a
 //    mismatching registration is dropped first;
-//  * registrations of unlinked files are dropped by sweep().
+//  * registrations of unlinked files are dropped by sweep();
+//  * only tmpfs files are registered (disk filesystems refuse long-term pins).
 #pragma once
 
 #include <sys/types.h>
