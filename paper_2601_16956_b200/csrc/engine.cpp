@@ -30,6 +30,17 @@ float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
+void mkdirs(const std::string& path) {
+  std::string cur;
+  for (size_t i = 0; i <= path.size(); ++i) {
+    if (i == path.size() || path[i] == '/') {
+      if (!cur.empty() && ::mkdir(cur.c_str(), 0755) != 0 && errno != EEXIST)
+        fail(TS_ERR_IO, "cannot create directory " + cur + ": " + std::strerror(errno));
+    }
+    if (i < path.size()) cur += path[i];
+  }
+}
+
 namespace {
 const bool g_trace = std::getenv("TS_TRACE") != nullptr;
 #define TRACE(...)                                                                     \
@@ -41,140 +52,7 @@ const bool g_trace = std::getenv("TS_TRACE") != nullptr;
     }                                                                                  \
   } while (0)
 
-void mkdirs(const std::string& path) {
-  std::string cur;
-  for (size_t i = 0; i <= path.size(); ++i) {
-    if (i == path.size() || path[i] == '/') {
-      if (!cur.empty() && ::mkdir(cur.c_str(), 0755) != 0 && errno != EEXIST)
-        fail(TS_ERR_IO, "cannot create directory " + cur + ": " + std::strerror(errno));
-    }
-    if (i < path.size()) cur += path[i];
-  }
-}
-std::chrono::steady_clock::time_point to_tp(int64_t ns) {
-  return std::chrono::steady_clock::time_point(std::chrono::nanoseconds(ns));
-}
 }  // namespace
-
-// ---------------------------------------------------------------------------
-// thread pool
-
-thread_pool::thread_pool(int n, std::function<void()> init) {
-  for (int i = 0; i < std::max(1, n); ++i)
-    threads_.emplace_back([this, init] {
-      if (init) init();
-      for (;;) {
-        std::function<void()> f;
-        {
-          std::unique_lock<std::mutex> g(mu_);
-          cv_.wait(g, [&] { return stop_ || !q_.empty(); });
-          if (q_.empty()) return;
-          f = std::move(q_.front());
-          q_.pop_front();
-        }
-        f();
-      }
-    });
-}
-
-thread_pool::~thread_pool() {
-  {
-    std::lock_guard<std::mutex> g(mu_);
-    stop_ = true;
-  }
-  cv_.notify_all();
-  for (auto& t : threads_) t.join();
-}
-
-void thread_pool::submit(std::function<void()> f) {
-  {
-    std::lock_guard<std::mutex> g(mu_);
-    q_.push_back([f = std::move(f)] {
-      try {
-        f();
-      } catch (const std::exception& e) {
-        std::fprintf(stderr, "ts_b200: uncaught exception in worker task: %s\n", e.what());
-      }
-    });
-  }
-  cv_.notify_one();
-}
-
-// ---------------------------------------------------------------------------
-// pinned pool (staging.cpp:10-115 semantics over cudaHostAlloc memory)
-
-pinned_pool::pinned_pool(uint64_t capacity) : capacity_(capacity) {
-  if (capacity == 0) fail(TS_ERR_GENERIC, "staging cache: zero capacity");
-  void* p = nullptr;
-  cuda_check(cudaHostAlloc(&p, capacity, cudaHostAllocPortable | cudaHostAllocMapped),
-             "cudaHostAlloc(staging pool)");
-  base_ = static_cast<uint8_t*>(p);
-}
-
-pinned_pool::~pinned_pool() {
-  if (base_) cudaFreeHost(base_);
-}
-
-bool pinned_pool::find_locked(uint64_t size, uint64_t* off) const {
-  auto free_at = [&](uint64_t start) {
-    if (start + size > capacity_) return false;
-    auto it = live_.lower_bound(start);
-    if (it != live_.end() && it->first < start + size) return false;
-    if (it != live_.begin()) {
-      auto prev = std::prev(it);
-      if (prev->first + prev->second > start) return false;
-    }
-    return true;
-  };
-  if (free_at(bump_)) return *off = bump_, true;
-  if (free_at(0)) return *off = 0, true;
-  uint64_t cursor = 0;
-  for (const auto& [o, l] : live_) {
-    if (o >= cursor && o - cursor >= size) return *off = cursor, true;
-    cursor = std::max(cursor, o + l);
-  }
-  if (capacity_ - cursor >= size) return *off = cursor, true;
-  return false;
-}
-
-pinned_pool::region pinned_pool::acquire(uint64_t size, int64_t deadline_ns) {
-  if (size == 0) fail(TS_ERR_GENERIC, "staging cache: zero-size acquire");
-  if (size > capacity_) fail(TS_ERR_GENERIC, "staging cache: oversized request");
-  std::unique_lock<std::mutex> g(mu_);
-  const uint64_t token = next_token_++;
-  waiters_.push_back(token);
-  for (;;) {
-    uint64_t off;
-    if (waiters_.front() == token && find_locked(size, &off)) {
-      waiters_.pop_front();
-      live_.emplace(off, size);
-      allocated_ += size;
-      peak_ = std::max(peak_, allocated_);
-      bump_ = (off + size) % capacity_;
-      cv_.notify_all();
-      return {next_id_++, off, size};
-    }
-    if (deadline_ns >= 0) {
-      if (now_ns() >= deadline_ns) {
-        waiters_.erase(std::find(waiters_.begin(), waiters_.end(), token));
-        cv_.notify_all();
-        fail(TS_ERR_CACHE_TIMEOUT, "staging cache: acquire deadline exceeded");
-      }
-      cv_.wait_until(g, to_tp(deadline_ns));
-    } else {
-      cv_.wait(g);
-    }
-  }
-}
-
-void pinned_pool::release(const region& r) {
-  std::lock_guard<std::mutex> g(mu_);
-  auto it = live_.find(r.offset);
-  if (it == live_.end()) fail(TS_ERR_GENERIC, "staging cache: release of unknown or freed region");
-  allocated_ -= it->second;
-  live_.erase(it);
-  cv_.notify_all();
-}
 
 // ---------------------------------------------------------------------------
 // ticket
@@ -1672,125 +1550,6 @@ void engine::file_progress(const std::shared_ptr<job>& j, size_t fi) {
   }
   j->t->cv.notify_all();
   f.w.reset();  // unmap + close after the waiters are released
-}
-
-// ---------------------------------------------------------------------------
-// session (engine.cpp:35-117): manifest written last, ranks sorted by id.
-
-manifest_rank make_rank_info(const ts_rank_info& rank, const ts_object_desc* objs, size_t n) {
-  manifest_rank info;
-  info.rank_id = rank.rank_id;
-  info.tp_idx = rank.tp_idx;
-  info.pp_idx = rank.pp_idx;
-  info.dp_idx = rank.dp_idx;
-  std::vector<uint32_t> fids;
-  for (size_t i = 0; i < n; ++i) fids.push_back(objs[i].file_id);
-  std::sort(fids.begin(), fids.end());
-  fids.erase(std::unique(fids.begin(), fids.end()), fids.end());
-  std::unordered_map<uint32_t, size_t> at;
-  for (uint32_t f : fids) {
-    at.emplace(f, info.files.size());
-    manifest_file mf;
-    mf.file_id = f;
-    mf.path = rank_dir_name(rank.rank_id) + "/file_" + std::to_string(f) + ".bin";
-    info.files.push_back(std::move(mf));
-  }
-  for (size_t i = 0; i < n; ++i) {
-    info.files[at.at(objs[i].file_id)].object_ids.push_back(objs[i].object_id);
-    info.objects.push_back({objs[i].object_id, objs[i].kind, objs[i].tier, objs[i].precision,
-                            objs[i].file_id});
-  }
-  return info;
-}
-
-session::session(const std::string& dir, uint64_t ckpt_id, uint64_t iteration,
-                 const ts_manifest_echo* echo, int n_ranks, bool writes)
-    : dir_(dir), n_ranks_(n_ranks), writes_(writes) {
-  m_.checkpoint_id = ckpt_id;
-  m_.iteration = iteration;
-  if (echo) {
-    m_.tp = echo->tp;
-    m_.pp = echo->pp;
-    m_.dp = echo->dp;
-    m_.zero1 = echo->zero1 != 0;
-    m_.seed = echo->seed;
-    m_.n_params = echo->n_params;
-    m_.layers = echo->layers;
-    m_.metadata_bytes = echo->metadata_bytes;
-  }
-  if (writes_ || !dir_.empty()) mkdirs(dir_);
-}
-
-void session::register_rank(manifest_rank info) {
-  std::lock_guard<std::mutex> g(mu_);
-  const int id = info.rank_id;
-  ranks_[id] = std::move(info);
-  persisted_.emplace(id, false);
-}
-
-std::vector<uint8_t> session::rank_blob(int rank_id) {
-  std::lock_guard<std::mutex> g(mu_);
-  auto it = ranks_.find(rank_id);
-  if (it == ranks_.end()) fail(TS_ERR_INVALID_ARG, "session: unknown rank");
-  return encode(rank_to_value(it->second));
-}
-
-void session::add_remote_rank(const uint8_t* blob, size_t n) {
-  manifest_rank r = rank_from_value(decode(blob, n));
-  std::unique_lock<std::mutex> g(mu_);
-  const int id = r.rank_id;
-  ranks_[id] = std::move(r);
-  persisted_[id] = true;
-  maybe_commit_locked(g);
-}
-
-void session::rank_persisted(int rank_id) {
-  std::unique_lock<std::mutex> g(mu_);
-  persisted_[rank_id] = true;
-  maybe_commit_locked(g);
-}
-
-void session::maybe_commit_locked(std::unique_lock<std::mutex>& g) {
-  int done = 0;
-  for (const auto& [id, p] : persisted_) done += p ? 1 : 0;
-  if (complete_ || committing_) return;
-  if (!writes_) {
-    if (done == static_cast<int>(persisted_.size())) {
-      complete_ = true;
-      cv_.notify_all();
-    }
-    return;
-  }
-  if (done < n_ranks_) return;
-  committing_ = true;
-  manifest m = m_;
-  m.complete = true;
-  for (const auto& [id, r] : ranks_) m.ranks.push_back(r);
-  g.unlock();
-  std::string err;
-  try {
-    write_manifest(dir_ + "/MANIFEST.tlv", m);
-  } catch (const error& e) {
-    err = e.what();
-  }
-  g.lock();
-  commit_error_ = err;
-  complete_ = true;
-  cv_.notify_all();
-  if (!err.empty()) fail(TS_ERR_IO, err);
-}
-
-bool session::wait_complete(int64_t timeout_ns) {
-  std::unique_lock<std::mutex> g(mu_);
-  if (timeout_ns < 0) cv_.wait(g, [&] { return complete_; });
-  else cv_.wait_for(g, std::chrono::nanoseconds(timeout_ns), [&] { return complete_; });
-  if (complete_ && !commit_error_.empty()) fail(TS_ERR_IO, commit_error_);
-  return complete_;
-}
-
-bool session::complete() {
-  std::lock_guard<std::mutex> g(mu_);
-  return complete_;
 }
 
 }  // namespace tsb

@@ -35,6 +35,8 @@
 namespace tsb {
 
 void cuda_check(cudaError_t e, const char* what);
+// mkdir -p
+void mkdirs(const std::string& path);
 // Elapsed time between two timing events, 0 (and no lingering error) if either was not recorded.
 float elapsed_ms(cudaEvent_t a, cudaEvent_t b);
 
