@@ -982,6 +982,15 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       }
       cuda_check(cudaEventRecord(pb, pack_stream_), "event");
       j->pack_events.push_back({pa, pb});
+      // Host-tier bytes join the staged image in stream order, before the
+      // capture event: the pre-update barrier then covers them too (copying
+      // them at window landing, after the barrier, let an update leak in).
+      for (size_t q = w; q < j->wins.size() && j->wins[q].lo < chi; ++q) {
+        const auto& wq = j->wins[shadow ? j->worder[q] : q];
+        for (uint32_t k = wq.hp_begin; k < wq.hp_end; ++k)
+          cuda_check(cudaMemcpyAsync(slot + (wq.lo + j->hp[k].win_off - clo), j->hp[k].src, j->hp[k].len,
+                                     cudaMemcpyHostToDevice, pack_stream_), "host-tier bytes to the staged image");
+      }
       cuda_check(cudaGetLastError(), "pack kernel launch");
       cudaEvent_t packed;
       cuda_check(cudaEventCreateWithFlags(&packed, cudaEventDisableTiming), "event");
@@ -1077,6 +1086,9 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       dev::launch_pack(d_segs, nsegs, win.lo, win.hi, dst, ctas, threads, pack_stream_);
       t.kernel_launches += 1;
       cuda_check(cudaGetLastError(), "pack kernel launch");
+      for (uint32_t k = win.hp_begin; k < win.hp_end; ++k)  // host-tier bytes, in stream order (capture)
+        cuda_check(cudaMemcpyAsync(win.host + j->hp[k].win_off, j->hp[k].src, j->hp[k].len, cudaMemcpyHostToHost,
+                                   pack_stream_), "host-tier bytes to the window");
       cuda_check(cudaEventRecord(win.ev, pack_stream_), "event");
       push_window(w);
     }
@@ -1104,6 +1116,9 @@ void engine::run_job(const std::shared_ptr<job>& j) {
           std::memset(dst + (a - win.lo), 0, b - a);
         }
       }
+      for (uint32_t k = win.hp_begin; k < win.hp_end; ++k)  // host-tier bytes, in stream order (capture)
+        cuda_check(cudaMemcpyAsync(dst + j->hp[k].win_off, j->hp[k].src, j->hp[k].len, cudaMemcpyHostToHost,
+                                   copy_stream_), "host-tier bytes to the window");
       cuda_check(cudaEventRecord(win.ev, copy_stream_), "event");
       push_window(w);
     }
@@ -1165,8 +1180,7 @@ void engine::window_landed(const std::shared_ptr<job>& j, size_t wi) {
   auto& w = j->wins[wi];
   TRACE("landed rank=%d w=%zu pieces=%u fsegs=%u", j->rank_id, wi, w.wp_end - w.wp_begin, w.fs_end - w.fs_begin);
   uint8_t* base = w.host;
-  for (uint32_t k = w.hp_begin; k < w.hp_end; ++k)
-    std::memcpy(base + j->hp[k].win_off, j->hp[k].src, j->hp[k].len);  // host-tier bytes
+  (void)base;  // (host-tier bytes were copied in stream order, as part of the capture)
   size_t newly_ready = 0;
   bool release_now = false;
   {
