@@ -28,6 +28,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# BASELINE.json's metric; `value` is the box GB/s, the blocked ms are in "blocked"
+METRIC = "checkpoint GB/s per GPU & box (1/2/4/8 B200); training blocked ms/ckpt"
 PCIE_D2H_MEASURED_GBPS = 57.2  # pinned cudaMemcpy D2H on this pool's B200 (gpurun_out/probe_box.json)
 
 
@@ -184,7 +186,7 @@ def reference_arm(args):
     if r is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ts_ref_driver not built"}))
         return
-    line = {"metric": "checkpoint snapshot GB/s (per GPU / box)", "impl": "reference", "value": round(r["value"], 4),
+    line = {"metric": METRIC, "impl": "reference", "value": round(r["value"], 4),
             "unit": "GB/s", "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
             "ms_per_step": round(1e3 * statistics.mean(r["snapshot_s"]), 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
@@ -516,7 +518,7 @@ def ours(args):
     clocks = clk.summary()
     if rank == 0:
         line = {
-            "metric": "checkpoint snapshot GB/s (per GPU / box)", "value": round(value, 3), "unit": "GB/s",
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(t_ms / args.steps, 2), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
