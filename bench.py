@@ -303,12 +303,14 @@ def ours(args):
                            checksum_on_gpu=not args.host_checksum, pack_kernel=args.pack_kernel,
                            checksum_priority=args.ck_priority, pack_priority=args.pack_priority,
                            checksum_host_frac=args.ck_host_frac, ring_chunk_bytes=int(args.ring_chunk_gb * (1 << 30)),
-                           worker_nice=args.worker_nice, helper_devices=helpers, helper_share=share)
+                           worker_nice=args.worker_nice, helper_devices=helpers, helper_share=share,
+                           flush_mmap=not args.flush_pwrite)
     eng = api.CheckpointEngine(cfg, spec.rank_id, local_dev)
     numa_node = eng.numa_node
     full = getattr(rec, "full_layout", None)
     echo = S.Recipe(layout=full).manifest_echo() if full else rec.manifest_echo()
-    tdir = os.path.join("/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir(), "ts_bench")
+    root = args.ckpt_root or ("/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir())
+    tdir = os.path.join(root, "ts_bench")
     if rank == 0:
         shutil.rmtree(tdir, ignore_errors=True)
         os.makedirs(tdir, exist_ok=True)
@@ -391,7 +393,13 @@ def ours(args):
                   f"(use --keep 1)", file=sys.stderr)
             args.e2e_steps = 0
     if args.e2e_steps > 0:
-        cfg_io = api.EngineConfig(**{**cfg.__dict__, "write_files": True})
+        io_kw = {"write_files": True}
+        if not os.path.realpath(root).startswith("/dev/shm") and not args.pool_gb:
+            # a disk filesystem takes no file_dma: windows wait in the pool for
+            # the (slower) page-cache flush, so give it the whole image when RAM allows
+            io_kw["staging_capacity_bytes"] = (min(img_est + (64 << 20), max(pool, int(0.3 * avail / max(1, local_ws)))
+                                               if avail else pool) + (2 << 20) - 1) // (2 << 20) * (2 << 20)
+        cfg_io = api.EngineConfig(**{**cfg.__dict__, **io_kw})
         eng.shutdown()
         eng_io = api.CheckpointEngine(cfg_io, spec.rank_id, local_dev)
         spare = os.path.join(tdir, ".spare")
@@ -437,9 +445,10 @@ def ours(args):
                "snapshot_ms_last": round(st["t_snapshot_ns"] / 1e6, 1),
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(image),
                "file_dma_frac": round(sum(dma) / (len(dma) * image), 3) if dma else 0.0,
-               "what": "issue -> files + footers + MANIFEST.tlv durable on /dev/shm, via the C-ABI"
-                       + ("" if args.fresh_files else f"; rotation keeps {args.keep} checkpoint(s), older files recycled, "
-                          "D2H windows land directly in their page-locked pages (file_dma)")}
+               "what": f"issue -> files + footers + MANIFEST.tlv written to {root} (page cache), via the C-ABI"
+                       + ("" if args.fresh_files else f"; rotation keeps {args.keep} checkpoint(s), older files recycled")
+                       + ("; D2H windows land directly in the files' page-locked pages (file_dma)" if sum(dma) else
+                          "; windows staged in the pinned pool, flushed by worker threads")}
         # restore of the last checkpoint (H2D + scatter-unpack + FNV verify)
         man = os.path.join(tdir, f"ckpt_{it:06d}", "MANIFEST.tlv")
         r = api.Restorer(man)
@@ -713,6 +722,8 @@ def main():
     ap.add_argument("--pack-priority", type=int, default=1, help="capture (pack) stream priority (1/0/-1)")
     ap.add_argument("--flush-workers", type=int, default=0, help="host worker threads (default: min(16, cores))")
     ap.add_argument("--keep", type=int, default=2, help="e2e rotation: checkpoints kept on tmpfs")
+    ap.add_argument("--ckpt-root", default="", help="e2e checkpoint directory root (default /dev/shm)")
+    ap.add_argument("--flush-pwrite", action="store_true", help="pool flushes with pwrite(2) instead of mmap copies")
     ap.add_argument("--no-train-files", dest="train_files", action="store_false",
                     help="training phase: snapshot only (no files)")
     ap.add_argument("--fresh-files", action="store_true",
