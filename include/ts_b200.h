@@ -232,6 +232,13 @@ typedef struct ts_manifest_echo {
  * allocating fresh page-cache pages. Same filesystem required. */
 ts_status ts_retire_checkpoint(const char* ckpt_dir, const char* spare_dir);
 ts_status ts_engine_set_spare_dir(ts_engine* e, const char* spare_dir);
+/* Creates up to `copies` spare files per file of the rank's layout in
+ * `spare_dir` (sized to tensor_region_end, page-locked when file_dma applies),
+ * so the first checkpoints of a rotation already take the direct D2H path.
+ * `locked_bytes` (may be NULL): bytes page-locked. */
+ts_status ts_engine_provision_spares(ts_engine* e, const char* spare_dir, const ts_rank_info* rank,
+                                     const ts_object_desc* objs, size_t n, int copies,
+                                     uint64_t* locked_bytes);
 /* Page-locked checkpoint files (ts_engine_config.file_dma): bytes currently
  * locked, and an explicit release of every idle registration (files of deleted
  * checkpoints are also released at the next issue). */

@@ -192,6 +192,8 @@ _sig("ts_engine_destroy", i32, P)
 _sig("ts_retire_checkpoint", i32, C.c_char_p, C.c_char_p)
 _sig("ts_engine_set_spare_dir", i32, P, C.c_char_p)
 _sig("ts_engine_numa_node", i32, P)
+_sig("ts_engine_provision_spares", i32, P, C.c_char_p, C.POINTER(RankInfo), C.POINTER(ObjectDesc), C.c_size_t,
+     i32, C.POINTER(C.c_uint64))
 _sig("ts_restore_set_file_cache", i32, P, i32)
 _sig("ts_file_cache_bytes", C.c_uint64)
 _sig("ts_file_cache_release_all", i32, C.POINTER(C.c_uint64))

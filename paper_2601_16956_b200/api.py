@@ -537,6 +537,18 @@ class CheckpointEngine:
         """NUMA node of the engine's threads and pinned pool (-1: none / single node)."""
         return int(N.lib.ts_engine_numa_node(self.h))
 
+    def provision_spares(self, spare_dir: str, rank: RankState, copies: int = 2) -> int:
+        """Spare files for this rank's layout in `spare_dir`, page-locked ahead of
+        time: with rotation, even the first checkpoints take the direct D2H.
+        Returns the bytes locked."""
+        keep: list = []
+        arr = _desc_array(rank, keep, need_payload=False)
+        info = N.RankInfo(rank.rank_id, rank.tp_idx, rank.pp_idx, rank.dp_idx)
+        out = C.c_uint64(0)
+        N.call(N.lib.ts_engine_provision_spares, self.h, spare_dir.encode(), C.byref(info), arr,
+               len(rank.objects), int(copies), C.byref(out))
+        return int(out.value)
+
     def set_spare_dir(self, spare_dir: str):
         """Take over files of checkpoints retired into `spare_dir` (retire_checkpoint)."""
         N.call(N.lib.ts_engine_set_spare_dir, self.h, spare_dir.encode())

@@ -240,6 +240,15 @@ ts_status ts_file_cache_release_all(uint64_t* released_bytes) {
   });
 }
 
+ts_status ts_engine_provision_spares(ts_engine* e, const char* spare_dir, const ts_rank_info* rank,
+                                     const ts_object_desc* objs, size_t n, int copies,
+                                     uint64_t* locked_bytes) {
+  return guard([&] {
+    const uint64_t b = e->e->provision_spares(spare_dir ? spare_dir : "", *rank, objs, n, copies);
+    if (locked_bytes) *locked_bytes = b;
+  });
+}
+
 int ts_engine_numa_node(ts_engine* e) { return e && e->e ? e->e->numa_node() : -1; }
 
 ts_status ts_engine_destroy(ts_engine* e) {

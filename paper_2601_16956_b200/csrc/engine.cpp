@@ -1,6 +1,7 @@
 // B200 snapshot engine (see engine.hpp for the reference mapping).
 #include "engine.hpp"
 
+#include <fcntl.h>
 #include <sys/resource.h>
 #include <sys/stat.h>
 #include <sys/syscall.h>
@@ -401,6 +402,48 @@ void* engine::ensure_seg_buffer(uint64_t bytes) {
   return segbuf_;
 }
 
+uint64_t engine::provision_spares(const std::string& spare_dir, const ts_rank_info& rank,
+                                  const ts_object_desc* objs, size_t n, int copies) {
+  const layout_plan plan = plan_layout(objs, n, cfg_.alignment);
+  mkdirs(spare_dir);
+  struct item {
+    int fd;
+    uint64_t len;
+  };
+  std::vector<item> made;
+  for (const auto& fp : plan.files) {
+    if (fp.tensor_region_end <= header_reserved) continue;
+    const std::string name = rank_dir_name(rank.rank_id) + "_file_" + std::to_string(fp.file_id) + ".bin";
+    int have = 0;
+    for (int k = 0; k < kMaxSpares; ++k)
+      have += ::access((spare_dir + "/" + name + (k ? "." + std::to_string(k) : std::string())).c_str(), F_OK) == 0;
+    for (int c = have; c < std::min(copies, kMaxSpares); ++c) {
+      const std::string p = spare_put_name(spare_dir, name);
+      const int fd = ::open(p.c_str(), O_RDWR | O_CREAT | O_EXCL, 0644);
+      if (fd < 0) fail(TS_ERR_IO, "cannot create spare " + p + ": " + std::strerror(errno));
+      if (::ftruncate(fd, static_cast<off_t>(fp.tensor_region_end)) != 0) {
+        ::close(fd);
+        fail(TS_ERR_IO, "cannot size spare " + p + ": " + std::strerror(errno));
+      }
+      made.push_back({fd, fp.tensor_region_end});
+    }
+  }
+  // Lock the new files' pages, one thread per file (page allocation + pinning).
+  std::atomic<uint64_t> locked{0};
+  std::vector<std::thread> th;
+  for (const auto& m : made)
+    th.emplace_back([&, m] {
+      file_key k;
+      if (cfg_.file_dma && file_registry::get().want_register(m.fd, m.len, &k)) {
+        file_registry::get().register_file(k, device_);
+        locked += m.len;
+      }
+    });
+  for (auto& t : th) t.join();
+  for (const auto& m : made) ::close(m.fd);
+  return locked.load();
+}
+
 // issue_checkpoint (engine.cpp:518-619), lazy by default.
 std::shared_ptr<ticket_state> engine::issue(const std::shared_ptr<session>& sp, const ts_rank_info& rank,
                                             const ts_object_desc* objs, size_t n,
@@ -477,8 +520,7 @@ std::shared_ptr<ticket_state> engine::issue(const std::shared_ptr<session>& sp, 
     fs.img = cursor;
     cursor += fp.tensor_region_end - header_reserved;
     const std::string fname = "file_" + std::to_string(fp.file_id) + ".bin";
-    const std::string recycled =
-        spare.empty() ? std::string() : spare + "/" + rank_dir_name(rank.rank_id) + "_" + fname;
+    const std::string recycled = spare.empty() ? std::string() : spare_take(spare, rank_dir_name(rank.rank_id) + "_" + fname);
     // Every opened file passes through the registry before it is truncated
     // (locked pages must never be dropped); a valid registration of exactly
     // [0, tre) makes the file's D2H windows land in its pages.

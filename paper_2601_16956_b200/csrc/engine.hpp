@@ -137,6 +137,11 @@ class engine {
     std::lock_guard<std::mutex> g(mu_);
     return spare_dir_;
   }
+  // Creates up to `copies` spare files per file of this rank's layout in
+  // `spare_dir` (sized, page-locked when file_dma applies), so the first
+  // checkpoints recycle them like later ones do. Returns the bytes locked.
+  uint64_t provision_spares(const std::string& spare_dir, const ts_rank_info& rank,
+                            const ts_object_desc* objs, size_t n, int copies);
   const ts_engine_config& config() const { return cfg_; }
   int device() const { return device_; }
   int numa_node() const { return numa_.node; }

@@ -299,6 +299,28 @@ std::vector<footer_entry> read_footer(const std::string& path, uint64_t* file_si
   return out;
 }
 
+namespace {
+std::string spare_name(const std::string& spare_dir, const std::string& name, int k) {
+  return spare_dir + "/" + name + (k ? "." + std::to_string(k) : std::string());
+}
+}  // namespace
+
+std::string spare_take(const std::string& spare_dir, const std::string& name) {
+  for (int k = 0; k < kMaxSpares; ++k) {
+    const std::string p = spare_name(spare_dir, name, k);
+    if (::access(p.c_str(), F_OK) == 0) return p;
+  }
+  return {};
+}
+
+std::string spare_put_name(const std::string& spare_dir, const std::string& name) {
+  for (int k = 0; k < kMaxSpares; ++k) {
+    const std::string p = spare_name(spare_dir, name, k);
+    if (::access(p.c_str(), F_OK) != 0) return p;
+  }
+  return spare_name(spare_dir, name, 0);  // full: replace the first
+}
+
 void retire_checkpoint(const std::string& dir, const std::string& spare_dir) {
   ::mkdir(spare_dir.c_str(), 0755);
   if (::unlink((dir + "/MANIFEST.tlv").c_str()) != 0 && errno != ENOENT)
@@ -318,7 +340,7 @@ void retire_checkpoint(const std::string& dir, const std::string& spare_dir) {
       if (std::strncmp(e->d_name, "file_", 5) == 0) files.push_back(e->d_name);
     ::closedir(rdh);
     for (const auto& f : files) {
-      const std::string dst = spare_dir + "/" + r + "_" + f;
+      const std::string dst = spare_put_name(spare_dir, r + "_" + f);
       if (::rename((rd + "/" + f).c_str(), dst.c_str()) != 0)
         fail(TS_ERR_IO, "cannot recycle " + rd + "/" + f + ": " + std::strerror(errno));
     }

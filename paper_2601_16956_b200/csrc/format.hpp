@@ -97,6 +97,13 @@ class file_writer {
 // freeing and re-faulting the page cache.
 void retire_checkpoint(const std::string& dir, const std::string& spare_dir);
 
+// Spare files of one name ("rank_0000_file_1.bin") may exist in up to
+// kMaxSpares copies (suffixes .1, .2, ...): retire adds one (the oldest surplus
+// is overwritten), an issue takes one, provisioning creates them ahead of time.
+constexpr int kMaxSpares = 4;
+std::string spare_take(const std::string& spare_dir, const std::string& name);  // "" if none
+std::string spare_put_name(const std::string& spare_dir, const std::string& name);
+
 struct file_header {
   uint32_t version;
   uint64_t plan_hash;

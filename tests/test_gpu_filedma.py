@@ -250,3 +250,44 @@ def test_fuzz_rotation_parity(gpu, shm, oracle, seed):
         assert read_tree(out) == read_tree(ref), (seed, k, cfg)
         shutil.rmtree(ref)
         prev = out
+
+
+@pytest.mark.parametrize("name", ["hand_mixed", "odd_layout", "two_ranks"])
+def test_provisioned_spares_first_checkpoint_direct(gpu, shm, oracle, name):
+    """provision_spares: the very first checkpoint of a rotation recycles
+    pre-created, page-locked spare files (direct D2H), byte-identical."""
+    rec = load(name)
+    spare = os.path.join(shm, "spare")
+    states = [api.materialize_payloads(r, 0, rec.pit) for r in rec.ranks]
+    engines = [api.CheckpointEngine(cfg_for("ring"), r.rank_id, 0) for r in rec.ranks]
+    locked = 0
+    for e, s in zip(engines, states):
+        e.set_spare_dir(spare)
+        locked += e.provision_spares(spare, s, copies=2)
+    assert locked >= fixed_bytes(rec, oracle)
+    out = os.path.join(shm, "c0")
+    session = api.CheckpointSession(out, rec.ckpt_id, rec.iteration, rec.manifest_echo(), n_ranks=len(rec.ranks))
+    tickets = [e.issue_checkpoint(session, s, rec.iteration) for e, s in zip(engines, states)]
+    for t in tickets:
+        t.wait_persisted()
+    session.wait_complete(60)
+    assert sum(t.stats()["file_dma_bytes"] for t in tickets) == fixed_bytes(rec, oracle)
+    for e in engines:
+        e.shutdown()
+    assert read_tree(out) == read_tree(os.path.join(GOLDEN, "trees", name))
+
+
+def test_spares_accumulate_up_to_limit(gpu, shm):
+    """retire_checkpoint keeps several spares per file name (suffixes), up to a cap."""
+    rec = load("odd_layout")
+    rotate(rec, shm, cfg_for("ring"), rounds=1)
+    spare = os.path.join(shm, "spare")
+    for k in range(6):  # retire 6 copies of the same checkpoint
+        d = os.path.join(shm, f"x{k}")
+        shutil.copytree(os.path.join(shm, "c0"), d)
+        api.retire_checkpoint(d, spare)
+    names = os.listdir(spare)
+    per = {}
+    for n in names:
+        per.setdefault(n.split(".bin")[0], []).append(n)
+    assert per and all(1 <= len(v) <= 4 for v in per.values())
