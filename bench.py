@@ -297,7 +297,7 @@ def ours(args):
     if avail:  # every rank of this node pins its pool: stay well inside host RAM
         pool_cap = min(pool_cap, max(1 << 30, int(0.3 * avail / max(1, local_ws))))
     pool = (min(img_est + (64 << 20), pool_cap) + (2 << 20) - 1) // (2 << 20) * (2 << 20)
-    cfg = api.EngineConfig(d2h_mode=args.mode, staging_capacity_bytes=pool, raw_chunk_bytes=64 << 20,
+    cfg = api.EngineConfig(d2h_mode=args.mode, staging_capacity_bytes=pool, raw_chunk_bytes=args.window_mb << 20,
                            device_staging_bytes=img_est + (1 << 20) if shadow else ring_bytes,
                            flush_workers=args.flush_workers or min(16, os.cpu_count() or 8), write_files=False,
                            checksum_on_gpu=not args.host_checksum, pack_kernel=args.pack_kernel,
@@ -724,6 +724,7 @@ def main():
     ap.add_argument("--keep", type=int, default=2, help="e2e rotation: checkpoints kept on tmpfs")
     ap.add_argument("--ckpt-root", default="", help="e2e checkpoint directory root (default /dev/shm)")
     ap.add_argument("--flush-pwrite", action="store_true", help="pool flushes with pwrite(2) instead of mmap copies")
+    ap.add_argument("--window-mb", type=int, default=64, help="D2H window (raw_chunk_bytes) in MiB")
     ap.add_argument("--no-train-files", dest="train_files", action="store_false",
                     help="training phase: snapshot only (no files)")
     ap.add_argument("--fresh-files", action="store_true",
