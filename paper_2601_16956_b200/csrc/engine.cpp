@@ -1221,8 +1221,9 @@ void engine::completer_loop() {
 void engine::window_landed(const std::shared_ptr<job>& j, size_t wi) {
   auto& w = j->wins[wi];
   TRACE("landed rank=%d w=%zu pieces=%u fsegs=%u", j->rank_id, wi, w.wp_end - w.wp_begin, w.fs_end - w.fs_begin);
+  // (host-tier bytes are already in the window: copied in stream order as part
+  // of the capture, never here after the barrier)
   uint8_t* base = w.host;
-  (void)base;  // (host-tier bytes were copied in stream order, as part of the capture)
   size_t newly_ready = 0;
   bool release_now = false;
   {

@@ -436,7 +436,6 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
   std::vector<uint32_t> dev_objs;
   for (uint32_t i = 0; i < objs.size(); ++i)
     if (objs[i].d->tier == TS_TIER_DEVICE) dev_objs.push_back(i);
-  uint64_t* d_states = nullptr;
   std::vector<uint64_t> dev_ck(dev_objs.size());
   if (!dev_objs.empty() && S.err_status == TS_OK) {
     std::vector<dev::fnv_obj> fo(dev_objs.size());
@@ -468,7 +467,6 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
     o.fnv = dev_ck[i];
     o.hashed = o.size;
   }
-  (void)d_states;
   const float h2d_ms = elapsed_ms(ev_a, ev_b);
   float unpack_ms = 0;
   for (auto& ue : unpack_ev) unpack_ms += elapsed_ms(ue.first, ue.second);
