@@ -388,7 +388,9 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
         continue;
       }
       ws->left = static_cast<int>(reads.size());
-      for (auto [k, x, y] : reads) {
+      for (const auto& rd : reads) {
+        const size_t k = std::get<0>(rd);
+        const uint64_t x = std::get<1>(rd), y = std::get<2>(rd);
         pool.submit([&, ws, k, x, y, lo, hi, slot, hs, direct] {
           try {
             pread_all(fds[k].fd, hs + (x - lo), y - x, header_reserved + (x - file_img[k].first), rc.files[k].path);
