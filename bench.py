@@ -98,7 +98,7 @@ def ncu_traffic(cfg: str, mode: str, pack_kernel: str):
             t = json.load(f)
     except Exception:
         return None
-    if t.get("workload") != cfg or mode != "ring" or pack_kernel != "warp":
+    if t.get("workload") != cfg or mode != "ring" or pack_kernel != t.get("pack_kernel", "warp"):
         return None
     return int(t["traffic_bytes_per_launch"])
 
@@ -715,7 +715,8 @@ def main():
                     help="synthetic fwd/bwd launched as one CUDA graph (default) or eagerly from Python")
     ap.add_argument("--ckpt-interval", type=int, default=1, help="checkpoint every k training steps")
     ap.add_argument("--host-checksum", action="store_true", help="FNV on host threads instead of the GPU kernels")
-    ap.add_argument("--pack-kernel", default="warp", choices=["warp", "bulk"])
+    ap.add_argument("--pack-kernel", default="bulk", choices=["warp", "bulk"],
+                    help="bulk: TMA cp.async.bulk for large 16-B aligned fragments + warp kernel for the rest")
     ap.add_argument("--ck-priority", type=int, default=-1, help="device checksum stream priority (1/0/-1)")
     ap.add_argument("--ck-host-frac", type=float, default=-1.0,
                     help="share of checksums on host workers (0: all GPU; <0: auto from host rate and cadence)")

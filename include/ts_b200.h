@@ -172,10 +172,10 @@ typedef struct ts_engine_config {
                                        device copy; 0: host threads over the pinned pool */
   int32_t flush_mmap;               /* 1 (default): fixed-region flushes copy into a shared mapping
                                        of the file (parallel per file); 0: pwrite(2) */
-  int32_t pack_kernel;              /* RING pack: 0 = warp gather kernel for everything;
-                                       1 = TMA bulk copies (cp.async.bulk through shared memory)
-                                       for 16-B aligned fragments >= bulk_min_bytes, warp kernel
-                                       for the rest */
+  int32_t pack_kernel;              /* RING pack: 1 (default) = TMA bulk copies (cp.async.bulk
+                                       through shared memory) for 16-B aligned fragments >=
+                                       bulk_min_bytes, warp kernel for the rest; 0 = warp gather
+                                       kernel for everything */
   uint64_t bulk_min_bytes;          /* default 1 MiB */
   int32_t file_dma;                 /* 1 (default): D2H windows land directly in page-locked
                                        file pages (cudaHostRegister of a shared mapping, tmpfs)

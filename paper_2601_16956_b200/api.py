@@ -330,7 +330,7 @@ class EngineConfig:
     write_files: bool = True
     checksum_on_gpu: bool = True
     flush_mmap: bool = True
-    pack_kernel: str = "warp"  # "warp" | "bulk" (TMA cp.async.bulk for large aligned fragments)
+    pack_kernel: str = "bulk"  # "bulk" (TMA cp.async.bulk for large aligned fragments + warp kernel) | "warp"
     bulk_min_bytes: int = 1 << 20
     file_dma: bool = True  # D2H straight into page-locked file pages when registered (rotation)
     checksum_priority: int = -1  # RING device checksums' stream: 1 high, 0 normal, -1 low (default)

@@ -195,7 +195,7 @@ void ts_engine_config_default(ts_engine_config* c) {
   c->write_files = 1;
   c->checksum_on_gpu = 1;
   c->flush_mmap = 1;
-  c->pack_kernel = 0;
+  c->pack_kernel = 1;
   c->bulk_min_bytes = 1ull << 20;
   c->file_dma = 1;
   c->checksum_priority = -1;

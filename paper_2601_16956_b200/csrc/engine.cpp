@@ -834,7 +834,8 @@ void engine::run_job(const std::shared_ptr<job>& j) {
   size_t nslots = 0, nchunks = 0;
   uint8_t* ring = nullptr;
   if (mode == TS_D2H_RING && j->img > 0) {
-    const uint64_t want = align_up(j->img, 256);
+    // (a whole number of bulk jobs, so the TMA path can run on a full shadow too)
+    const uint64_t want = align_up(j->img, cfg_.pack_kernel == 1 ? static_cast<uint64_t>(dev::kBulkJob) : 256);
     const uint64_t cap = std::max<uint64_t>(cfg_.device_staging_bytes, 2 * W);
     if (cap >= want) {
       chunk = want;

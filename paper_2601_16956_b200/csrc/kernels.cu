@@ -283,6 +283,8 @@ __global__ void __launch_bounds__(32) pack_bulk_kernel(const bulk_job* __restric
                                                        uint64_t lo, uint8_t* dst) {
   extern __shared__ __align__(128) uint8_t stage_buf[];
   __shared__ __align__(8) uint64_t bars[kBulkStages];
+  __shared__ uint64_t st_dst[kBulkStages];  // store target / length of each stage, kept from its
+  __shared__ uint32_t st_len[kBulkStages];  // issue: no dependent global load on the store path
   if (threadIdx.x != 0) return;
   const uint32_t first = blockIdx.x, step = gridDim.x;
   const uint32_t mine = first < njobs ? (njobs - first + step - 1) / step : 0;
@@ -290,11 +292,17 @@ __global__ void __launch_bounds__(32) pack_bulk_kernel(const bulk_job* __restric
   for (int s = 0; s < kBulkStages; ++s)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[s])));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  // job descriptors are read one issue ahead, so their load latency overlaps
+  // the bulk copies instead of sitting on the single issuing thread's path
+  bulk_job next = jobs[first];
   auto issue = [&](uint32_t i) {
-    const bulk_job& jb = jobs[first + i * step];
+    const bulk_job jb = next;
+    if (i + 1 < mine) next = jobs[first + (i + 1) * step];
     const int s = static_cast<int>(i % kBulkStages);
     const uint32_t bar = smem_u32(&bars[s]);
     const uint32_t len = static_cast<uint32_t>(jb.len);
+    st_dst[s] = jb.pos - lo;
+    st_len[s] = len;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(len) : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_u32(stage_buf + s * kBulkJob)), "l"(jb.src), "r"(len), "r"(bar) : "memory");
@@ -308,9 +316,8 @@ __global__ void __launch_bounds__(32) pack_bulk_kernel(const bulk_job* __restric
     while (!done)
       asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
                    : "=r"(done) : "r"(bar), "r"(parity) : "memory");
-    const bulk_job& jb = jobs[first + i * step];
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                 ::"l"(dst + (jb.pos - lo)), "r"(smem_u32(stage_buf + s * kBulkJob)), "r"(static_cast<uint32_t>(jb.len))
+                 ::"l"(dst + st_dst[s]), "r"(smem_u32(stage_buf + s * kBulkJob)), "r"(st_len[s])
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     if (i + kBulkStages - 1 < mine) {
