@@ -546,7 +546,8 @@ def ours(args):
             "d2h_gbps": round(image / (statistics.mean(d2h_ms) / 1e3) / 1e9, 3) if min(d2h_ms) > 0 else None,
             "d2h_frac_pcie": round(image / (statistics.mean(d2h_ms) / 1e3) / 1e9 / PCIE_D2H_MEASURED_GBPS, 3)
             if min(d2h_ms) > 0 else None,
-            "roofline": {"kernel": "pack_kernel" if args.mode != "direct" else "copy-engine DMA",
+            "roofline": {"kernel": ("pack_bulk_kernel (TMA) + pack_kernel" if args.pack_kernel == "bulk" else "pack_kernel")
+                         if args.mode != "direct" else "copy-engine DMA",
                          "bound": "hbm", "achieved": round(pack_alg / (pack_mean / 1e3) / 1e9, 1),
                          "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(pack_alg / (pack_mean / 1e3) / 1e9 / hbm_peak, 3),
