@@ -250,6 +250,10 @@ engine::engine(const ts_engine_config& cfg, int rank_id, int device)
   // capture path and may run at a lower priority than the pack.
   const int ck_prio = cfg_.checksum_priority > 0 ? hi_prio : cfg_.checksum_priority < 0 ? lo_prio : 0;
   cuda_check(cudaStreamCreateWithPriority(&ck_stream_, cudaStreamNonBlocking, ck_prio), "stream");
+  // ...except where the capture depends on them: a ring slot is repacked only
+  // after its checksums, so those run at the pack's priority (at low priority
+  // they starve behind back-to-back training kernels and stall the capture)
+  cuda_check(cudaStreamCreateWithPriority(&ck_hi_stream_, cudaStreamNonBlocking, pack_prio), "stream");
   // Workers (checksums, flushes, serialization, page locking) are background
   // work: a lower CPU priority keeps the training process's kernel-launching
   // thread responsive when every core is hashing.
@@ -295,6 +299,7 @@ engine::~engine() {
   if (ck_host_) cudaFreeHost(ck_host_);
   if (pack_stream_) cudaStreamDestroy(pack_stream_);
   if (ck_stream_) cudaStreamDestroy(ck_stream_);
+  if (ck_hi_stream_) cudaStreamDestroy(ck_hi_stream_);
   for (auto& h : helpers_) {
     cudaSetDevice(h->dev);
     for (auto e : h->free_ev) cudaEventDestroy(e);
@@ -862,7 +867,11 @@ void engine::run_job(const std::shared_ptr<job>& j) {
   const std::vector<dev::seg>* segs_for_warp = &j->segs;
   // (chunks must be kBulkJob multiples so that no job straddles two ring slots;
   // with odd window sizes the warp kernel does everything)
-  if (use_ring && cfg_.pack_kernel == 1 && chunk % dev::kBulkJob == 0) {
+  // Only for a full device shadow (one pack of the whole image): in a ring of
+  // slots every chunk's pack is issued while training kernels run, and the
+  // bulk kernel's CTAs (192 KiB of shared memory each) then wait for whole SMs
+  // — measured: cfg4 with a ring, 22 % step slowdown with bulk vs 4 % warp.
+  if (use_ring && nslots == 1 && cfg_.pack_kernel == 1 && chunk % dev::kBulkJob == 0) {
     for (const auto& sg : j->segs) {
       const uint64_t body = sg.len & ~15ull;
       const bool bulk = sg.src && (reinterpret_cast<uintptr_t>(sg.src) & 15) == 0 && (sg.pos & 15) == 0 &&
@@ -1045,11 +1054,23 @@ void engine::run_job(const std::shared_ptr<job>& j) {
         ~ev_guard() { cudaEventDestroy(e); }
       } packed_guard{packed};
       if (nf) {  // reads the slot on the checksum stream, overlapping the D2H
-        cuda_check(cudaStreamWaitEvent(ck_stream_, packed, 0), "wait pack");
-        launch_checksums(c, ck_stream_);
+        // chunks whose slot is packed again in this job: capture path, pack
+        // priority; the last ring-full: low priority (chained states keep the
+        // launches in chunk order across the two streams)
+        const bool reused = c + nslots < nchunks;
+        cudaStream_t cs = reused ? ck_hi_stream_ : ck_stream_;
+        if (!reused && c > 0 && c - 1 + nslots < nchunks) {  // first low-priority chunk after high ones
+          cudaEvent_t hand;
+          cuda_check(cudaEventCreateWithFlags(&hand, cudaEventDisableTiming), "event");
+          cuda_check(cudaEventRecord(hand, ck_hi_stream_), "event");
+          cuda_check(cudaStreamWaitEvent(ck_stream_, hand, 0), "checksum order");
+          cudaEventDestroy(hand);
+        }
+        cuda_check(cudaStreamWaitEvent(cs, packed, 0), "wait pack");
+        launch_checksums(c, cs);
         cudaEvent_t ck;
         cuda_check(cudaEventCreateWithFlags(&ck, cudaEventDisableTiming), "event");
-        cuda_check(cudaEventRecord(ck, ck_stream_), "event");
+        cuda_check(cudaEventRecord(ck, cs), "event");
         j->ck_events[c] = ck;
       }
       std::vector<char> helper_used(helpers_.size(), 0);

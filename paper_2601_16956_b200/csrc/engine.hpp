@@ -183,6 +183,7 @@ class engine {
   std::unique_ptr<pinned_pool> pool_;
   std::unique_ptr<thread_pool> workers_;
   cudaStream_t pack_stream_ = nullptr, copy_stream_ = nullptr, ck_stream_ = nullptr;
+  cudaStream_t ck_hi_stream_ = nullptr;  // checksums a ring slot's reuse (hence the capture) waits for
   uint8_t* ring_ = nullptr;
   uint64_t ring_bytes_ = 0;
   void* segbuf_ = nullptr;
