@@ -570,6 +570,13 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
     import torch
 
     run, fb_ms = gemm_load(args.fwd_bwd_ms, dev, graph=args.fwd_bwd == "graph")
+    # Long-lived objects (thousands of state descriptors) out of the cyclic GC's
+    # reach, as training loops do: a full collection over them landed inside
+    # random issue calls (up to ~270 ms for cfg4's 3,616 objects).
+    import gc
+
+    gc.collect()
+    gc.freeze()
     # Checkpoints go where a deployment puts them: files on tmpfs with rotation
     # (keep `--keep`, file_dma), when tmpfs has room; else snapshot-only.
     ws, rank, _ = dist_info()
