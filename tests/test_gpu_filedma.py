@@ -32,9 +32,11 @@ def shm():
 def cfg_for(mode, **kw):
     extra = {}
     if mode == "ring-bulk":
-        mode, extra = "ring", dict(pack_kernel="bulk", bulk_min_bytes=32768)
+        # (a full device shadow: the bulk path is used for one-pack images only)
+        mode, extra = "ring", dict(pack_kernel="bulk", bulk_min_bytes=32768, device_staging_bytes=256 << 20)
     base = dict(d2h_mode=mode, raw_chunk_bytes=64 << 10, staging_capacity_bytes=1 << 20,
-                device_staging_bytes=256 << 10, flush_workers=3, **extra)
+                device_staging_bytes=256 << 10, flush_workers=3)
+    base.update(extra)
     base.update(kw)
     return api.EngineConfig(**base)
 
