@@ -246,3 +246,21 @@ def test_helper_gpu_d2h_identical(gpu, tmp_path, name, staging, share):
     assert 0 < helper <= image
     if share == 1.0:
         assert helper == image or helper >= image - (64 << 10)  # every window (padding never moves)
+
+
+@pytest.mark.parametrize("name", ["hand_mixed", "odd_layout", "tiny_layout", "nozero_dp2"])
+def test_bulk_path_engaged_on_shadow(gpu, tmp_path, name):
+    """With a full device shadow the TMA bulk kernel carries the large aligned
+    fragments (one extra launch per rank) and the bytes stay identical; in a
+    multi-slot ring only the warp kernel runs."""
+    rec = S.load_recipe(os.path.join(GOLDEN, "recipes", name + ".recipe"))
+    launches = {}
+    for label, kw in (("warp", dict(pack_kernel="warp", device_staging_bytes=256 << 20)),
+                      ("bulk", dict(pack_kernel="bulk", bulk_min_bytes=32768, device_staging_bytes=256 << 20)),
+                      ("ring", dict(pack_kernel="bulk", bulk_min_bytes=32768))):
+        out = str(tmp_path / label)
+        _, _, stats, _ = checkpoint_recipe(rec, out, cfg_for("ring", **kw))
+        assert read_tree(out) == read_tree(os.path.join(GOLDEN, "trees", name))
+        launches[label] = sum(s["kernel_launches"] for s in stats)
+    ranks_with_big = sum(1 for r in rec.ranks if any(o.kind == 0 and o.tier == 0 and o.size >= 32768 for o in r.objects))
+    assert launches["bulk"] == launches["warp"] + ranks_with_big
