@@ -36,7 +36,7 @@ uint64_t g_pinned_bytes = 0;
 
 // Device window ring, per device, grown on demand and kept (stream-ordered
 // frees of a multi-GB buffer return it to the OS at the next sync: slow).
-std::unordered_map<int, std::pair<uint8_t*, uint64_t>> g_dev_stage, g_dev_scratch;
+std::unordered_map<int, std::pair<uint8_t*, uint64_t>> g_dev_stage, g_dev_scratch, g_dev_fnv;
 uint8_t* device_cached(std::unordered_map<int, std::pair<uint8_t*, uint64_t>>& m, int device, uint64_t bytes) {
   auto& e = m[device];
   if (e.second < bytes) {
@@ -50,6 +50,7 @@ uint8_t* device_cached(std::unordered_map<int, std::pair<uint8_t*, uint64_t>>& m
 }
 uint8_t* device_stage(int device, uint64_t bytes) { return device_cached(g_dev_stage, device, bytes); }
 uint8_t* device_scratch(int device, uint64_t bytes) { return device_cached(g_dev_scratch, device, bytes); }
+uint8_t* device_fnv(int device, uint64_t bytes) { return device_cached(g_dev_fnv, device, bytes); }
 
 uint8_t* pinned_stage(uint64_t bytes) {
   if (g_pinned_bytes < bytes) {
@@ -190,10 +191,20 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
 
   // Device scatter table (device-tier destinations only).
   std::vector<dev::useg> usegs;
+  std::vector<uint32_t> useg_dev;  // per scatter segment: index of its object among device-tier objects
+  std::vector<uint32_t> dev_objs;
+  std::vector<int64_t> dev_index(objs.size(), -1);
+  for (uint32_t i = 0; i < objs.size(); ++i)
+    if (objs[i].d->tier == TS_TIER_DEVICE) {
+      dev_index[i] = static_cast<int64_t>(dev_objs.size());
+      dev_objs.push_back(i);
+    }
   for (const auto& p : pieces) {
     const auto& o = objs[p.obj];
-    if (o.d->tier == TS_TIER_DEVICE)
+    if (o.d->tier == TS_TIER_DEVICE) {
       usegs.push_back({p.pos, p.len, static_cast<uint8_t*>(const_cast<void*>(o.d->data)) + p.obj_off});
+      useg_dev.push_back(static_cast<uint32_t>(dev_index[p.obj]));
+    }
   }
 
   // Pipeline: K pinned windows of W bytes. Reads of a window are cut in 16 MiB
@@ -222,6 +233,64 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
   cudaEvent_t ev_a, ev_b;
   cudaEventCreate(&ev_a);
   cudaEventCreate(&ev_b);
+
+  // Device checksums over the restored shards (the whole chain file -> pinned
+  // -> H2D -> unpack), window by window in image order on their own stream:
+  // chained per-object states, so they overlap the remaining transfers instead
+  // of following them. Tables are built up front; the sequencer below launches
+  // window w once it is unpacked and every earlier window has been launched.
+  const uint32_t nf = static_cast<uint32_t>(dev_objs.size());
+  const uint64_t nwin = img ? (img + W - 1) / W : 0;
+  struct fnv_window {
+    std::vector<dev::fnv_obj> fo;
+    uint64_t nseg = 0, nchunk = 0;
+  };
+  std::vector<fnv_window> fwin(nwin);
+  uint64_t max_tab = 0, max_scr = 0;
+  for (uint64_t w = 0; w < nwin; ++w) {
+    const uint64_t lo = w * W, hi = std::min(img, lo + W);
+    auto uit = std::lower_bound(usegs.begin(), usegs.end(), lo,
+                                [](const dev::useg& u, uint64_t x) { return u.pos + u.len <= x; });
+    for (; uit != usegs.end() && uit->pos < hi; ++uit) {
+      const uint64_t a = std::max(lo, uit->pos), b = std::min(hi, uit->pos + uit->len);
+      if (b > a) fwin[w].fo.push_back({uit->dst + (a - uit->pos), b - a, 0, 0, useg_dev[uit - usegs.begin()]});
+    }
+    auto& fw = fwin[w];
+    if (fw.fo.empty()) continue;
+    fw.nseg = dev::fnv_prepare(fw.fo.data(), static_cast<uint32_t>(fw.fo.size()), &fw.nchunk);
+    max_tab = std::max<uint64_t>(max_tab, fw.fo.size() * sizeof(dev::fnv_obj));
+    max_scr = std::max<uint64_t>(max_scr, dev::fnv_scratch_bytes(fw.nseg, fw.nchunk, static_cast<uint32_t>(fw.fo.size())));
+  }
+  const uint64_t st_b = align_up(std::max<uint64_t>(nf, 1) * 8ull, 256), tab_b = align_up(std::max<uint64_t>(max_tab, 1), 256);
+  uint8_t* fbuf = device_fnv(device, st_b + tab_b + max_scr);
+  uint64_t* d_states = reinterpret_cast<uint64_t*>(fbuf);
+  dev::fnv_obj* d_tab = reinterpret_cast<dev::fnv_obj*>(fbuf + st_b);
+  uint8_t* d_scr = fbuf + st_b + tab_b;
+  struct stream_guard {
+    cudaStream_t s = nullptr;
+    ~stream_guard() {
+      if (s) cudaStreamDestroy(s);
+    }
+  } fst;
+  cuda_check(cudaStreamCreateWithFlags(&fst.s, cudaStreamNonBlocking), "checksum stream");
+  const std::vector<uint64_t> seeds(std::max<uint32_t>(nf, 1), fnv_seed);
+  if (nf) cuda_check(cudaMemcpyAsync(d_states, seeds.data(), nf * 8ull, cudaMemcpyHostToDevice, fst.s), "upload");
+  std::vector<cudaEvent_t> win_unpacked(nwin, nullptr);
+  std::vector<char> win_ready(nwin, 0);
+  uint64_t next_fnv = 0;
+  std::atomic<uint32_t> launches_f{0};
+  auto fnv_advance = [&]() {  // under cuda_mu
+    for (; next_fnv < nwin && win_ready[next_fnv]; ++next_fnv) {
+      auto& fw = fwin[next_fnv];
+      if (fw.fo.empty()) continue;
+      cuda_check(cudaStreamWaitEvent(fst.s, win_unpacked[next_fnv], 0), "checksums wait for the unpack");
+      cuda_check(cudaMemcpyAsync(d_tab, fw.fo.data(), fw.fo.size() * sizeof(dev::fnv_obj), cudaMemcpyHostToDevice,
+                                 fst.s), "upload checksum table");
+      dev::launch_fnv(d_tab, static_cast<uint32_t>(fw.fo.size()), fw.nseg, fw.nchunk, d_states, d_scr, fst.s);
+      launches_f += 11;
+      cuda_check(cudaGetLastError(), "checksum kernels");
+    }
+  };
 
   std::vector<fd_holder> fds(rc.files.size());
   for (size_t k = 0; k < rc.files.size(); ++k) {
@@ -336,7 +405,10 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
       unpack_ev.emplace_back(u0, u1);
       launches_a += 1;
       cuda_check(cudaGetLastError(), "unpack launch");
+      win_unpacked[lo / W] = u1;
     }
+    win_ready[lo / W] = 1;
+    fnv_advance();
     cuda_check(cudaLaunchHostFunc(st, [](void* a) {
                  auto* p = static_cast<host_cb_arg*>(a);
                  std::lock_guard<std::mutex> g(p->s->mu);
@@ -433,34 +505,13 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
     }
   }
   cuda_check(cudaEventRecord(ev_b, st), "event");
-  // Device-tier objects: exact FNV kernels over the restored shards themselves
-  // (checks the whole chain file -> pinned -> H2D -> unpack).
-  std::vector<uint32_t> dev_objs;
-  for (uint32_t i = 0; i < objs.size(); ++i)
-    if (objs[i].d->tier == TS_TIER_DEVICE) dev_objs.push_back(i);
   std::vector<uint64_t> dev_ck(dev_objs.size());
-  if (!dev_objs.empty() && S.err_status == TS_OK) {
-    std::vector<dev::fnv_obj> fo(dev_objs.size());
-    std::vector<uint64_t> seeds(dev_objs.size(), fnv_seed);
-    for (size_t i = 0; i < dev_objs.size(); ++i) {
-      const auto& o = objs[dev_objs[i]];
-      fo[i] = {static_cast<const uint8_t*>(o.d->data), o.size, 0, 0, i};
-    }
-    const uint32_t nf = static_cast<uint32_t>(fo.size());
-    uint64_t nchunk = 0;
-    const uint64_t nseg = dev::fnv_prepare(fo.data(), nf, &nchunk);
-    const uint64_t tb = align_up(nf * sizeof(dev::fnv_obj), 256), sb = align_up(nf * 8ull, 256);
-    // Checksums run after the last unpack: the scatter table's scratch can be reused.
-    cuda_check(cudaStreamSynchronize(st), "restore stream");
-    uint8_t* fb = device_scratch(device, tb + sb + dev::fnv_scratch_bytes(nseg, nchunk, nf));
-    cuda_check(cudaMemcpyAsync(fb, fo.data(), nf * sizeof(dev::fnv_obj), cudaMemcpyHostToDevice, st), "upload");
-    cuda_check(cudaMemcpyAsync(fb + tb, seeds.data(), nf * 8ull, cudaMemcpyHostToDevice, st), "upload");
-    dev::launch_fnv(reinterpret_cast<dev::fnv_obj*>(fb), nf, nseg, nchunk, reinterpret_cast<uint64_t*>(fb + tb),
-                    fb + tb + sb, st);
-    launches += 11;
-    cuda_check(cudaGetLastError(), "checksum kernels");
-    cuda_check(cudaMemcpyAsync(dev_ck.data(), fb + tb, nf * 8ull, cudaMemcpyDeviceToHost, st), "download");
-  }
+  if (S.err_status == TS_OK && next_fnv != nwin)
+    fail(TS_ERR_GENERIC, "restore: device checksums did not cover every window");
+  if (nf && S.err_status == TS_OK)
+    cuda_check(cudaMemcpyAsync(dev_ck.data(), d_states, nf * 8ull, cudaMemcpyDeviceToHost, fst.s), "download");
+  cuda_check(cudaStreamSynchronize(fst.s), "checksum stream");
+  launches += launches_f.load();
   rtrace("pipeline done", t_begin);
   cuda_check(cudaStreamSynchronize(st), "restore stream");
   rtrace("device checksums done", t_begin);
