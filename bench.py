@@ -304,7 +304,7 @@ def ours(args):
                            checksum_priority=args.ck_priority, pack_priority=args.pack_priority,
                            checksum_host_frac=args.ck_host_frac, ring_chunk_bytes=int(args.ring_chunk_gb * (1 << 30)),
                            worker_nice=args.worker_nice, helper_devices=helpers, helper_share=share,
-                           flush_mmap=not args.flush_pwrite)
+                           flush_mmap=2 if args.flush_direct else int(not args.flush_pwrite))
     eng = api.CheckpointEngine(cfg, spec.rank_id, local_dev)
     numa_node = eng.numa_node
     full = getattr(rec, "full_layout", None)
@@ -422,7 +422,7 @@ def ours(args):
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
-        dma = []
+        dma, dio = [], []
         for _ in range(args.e2e_steps):
             it += 1
             # rotation: keep the last `keep` checkpoints, recycle older files
@@ -433,6 +433,7 @@ def ours(args):
                 dist.barrier()
             st, sess = step(it, eng_io, True)
             dma.append(st["file_dma_bytes"])
+            dio.append(st["direct_io_bytes"])
         f1.record()
         torch.cuda.synchronize()
         e2e_ms = f0.elapsed_time(f1)
@@ -445,6 +446,7 @@ def ours(args):
                "snapshot_ms_last": round(st["t_snapshot_ns"] / 1e6, 1),
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(image),
                "file_dma_frac": round(sum(dma) / (len(dma) * image), 3) if dma else 0.0,
+               "direct_io_frac": round(sum(dio) / (len(dio) * image), 3) if dio else 0.0,
                "what": f"issue -> files + footers + MANIFEST.tlv written to {root} (page cache), via the C-ABI"
                        + ("" if args.fresh_files else f"; rotation keeps {args.keep} checkpoint(s), older files recycled")
                        + ("; D2H windows land directly in the files' page-locked pages (file_dma)" if sum(dma) else
@@ -733,6 +735,8 @@ def main():
     ap.add_argument("--keep", type=int, default=2, help="e2e rotation: checkpoints kept on tmpfs")
     ap.add_argument("--ckpt-root", default="", help="e2e checkpoint directory root (default /dev/shm)")
     ap.add_argument("--flush-pwrite", action="store_true", help="pool flushes with pwrite(2) instead of mmap copies")
+    ap.add_argument("--flush-direct", action="store_true",
+                    help="pool flushes with O_DIRECT pwrite from the pinned windows (disk filesystems)")
     ap.add_argument("--window-mb", type=int, default=64, help="D2H window (raw_chunk_bytes) in MiB")
     ap.add_argument("--no-train-files", dest="train_files", action="store_false",
                     help="training phase: snapshot only (no files)")

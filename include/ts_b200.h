@@ -171,7 +171,10 @@ typedef struct ts_engine_config {
   int32_t checksum_on_gpu;          /* 1 (default): exact segment-parallel FNV-1a kernels on the
                                        device copy; 0: host threads over the pinned pool */
   int32_t flush_mmap;               /* 1 (default): fixed-region flushes copy into a shared mapping
-                                       of the file (parallel per file); 0: pwrite(2) */
+                                       of the file (parallel per file); 0: pwrite(2); 2: O_DIRECT
+                                       pwrite of each window's 4 KiB-aligned body straight from the
+                                       pinned pool (page cache bypassed; disks), buffered where
+                                       the filesystem refuses O_DIRECT (tmpfs) */
   int32_t pack_kernel;              /* RING pack: 1 (default) = TMA bulk copies (cp.async.bulk
                                        through shared memory) for 16-B aligned fragments >=
                                        bulk_min_bytes, warp kernel for the rest; 0 = warp gather
@@ -293,6 +296,7 @@ typedef struct ts_ticket_stats {
   uint64_t file_dma_bytes; /* fixed-region bytes the copy engines wrote straight into file pages */
   uint64_t host_checksum_bytes; /* device-tier bytes hashed by host workers (rest: FNV kernels) */
   uint64_t helper_bytes;        /* image bytes D2H'd by helper GPUs (helper_mask) */
+  uint64_t direct_io_bytes;     /* fixed-region bytes written with O_DIRECT (flush_mmap = 2) */
 } ts_ticket_stats;
 ts_status ts_ticket_stats_get(ts_ticket* t, ts_ticket_stats* out);
 /* Per-object checksum accumulated at staging (transfer.cpp:163-166) */

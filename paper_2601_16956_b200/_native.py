@@ -121,7 +121,8 @@ class TicketStats(C.Structure):
                 ("pack_ms", C.c_float), ("d2h_ms", C.c_float), ("kernel_launches", C.c_uint32),
                 ("copies", C.c_uint32), ("snapshot_done", C.c_int32), ("persisted_done", C.c_int32),
                 ("failed", C.c_int32), ("file_dma_bytes", C.c_uint64),
-                ("host_checksum_bytes", C.c_uint64), ("helper_bytes", C.c_uint64)]
+                ("host_checksum_bytes", C.c_uint64), ("helper_bytes", C.c_uint64),
+                ("direct_io_bytes", C.c_uint64)]
 
 
 class RestoreObject(C.Structure):

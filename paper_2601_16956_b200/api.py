@@ -329,7 +329,7 @@ class EngineConfig:
     pack_priority: int = 1  # capture stream: 1 high (default), 0 normal, -1 low
     write_files: bool = True
     checksum_on_gpu: bool = True
-    flush_mmap: bool = True
+    flush_mmap: int = 1  # 1: copy into a shared mapping; 0: pwrite; 2: O_DIRECT body + pwrite head/tail
     pack_kernel: str = "bulk"  # "bulk" (TMA cp.async.bulk for large aligned fragments + warp kernel) | "warp"
     bulk_min_bytes: int = 1 << 20
     file_dma: bool = True  # D2H straight into page-locked file pages when registered (rotation)

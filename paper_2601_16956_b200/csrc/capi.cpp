@@ -370,6 +370,7 @@ ts_status ts_ticket_stats_get(ts_ticket* t, ts_ticket_stats* o) {
     o->file_dma_bytes = s.file_dma_bytes;
     o->host_checksum_bytes = s.host_checksum_bytes;
     o->helper_bytes = s.helper_bytes;
+    o->direct_io_bytes = s.direct_io_bytes;
   });
 }
 

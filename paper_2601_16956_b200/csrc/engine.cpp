@@ -544,7 +544,8 @@ std::shared_ptr<ticket_state> engine::issue(const std::shared_ptr<session>& sp, 
     fs.w = std::make_unique<file_writer>(rdir + "/" + fname, fp.tensor_region_end, j->plan.hash,
                                          cfg_.overwrite != 0, j->io, recycled, on_open);
     fs.append_end = fp.tensor_region_end;
-    if (cfg_.flush_mmap && !fs.dma) fs.w->map_fixed_region();
+    if (cfg_.flush_mmap == 2 && !fs.dma) fs.w->open_direct();
+    else if (cfg_.flush_mmap && !fs.dma) fs.w->map_fixed_region();
     fidx.emplace(fp.file_id, static_cast<uint32_t>(j->files.size()));
     j->files.push_back(std::move(fs));
   }
@@ -1590,6 +1591,10 @@ void engine::file_progress(const std::shared_ptr<job>& j, size_t fi) {
   } catch (const error& e) {
     j->t->fail(e.status, std::string("finalize failed: ") + e.what(), e.object_id);
     return;
+  }
+  if (const uint64_t d = f.w->direct_bytes()) {
+    std::lock_guard<std::mutex> g(j->t->mu);
+    j->t->direct_io_bytes += d;
   }
   if (j->io && f.w->fd() >= 0) {
     // Locked-page bookkeeping: stamp a used registration; with rotation on,

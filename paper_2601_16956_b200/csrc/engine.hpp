@@ -102,6 +102,7 @@ struct ticket_state {
   uint64_t file_dma_bytes = 0;  // fixed-region bytes DMA'd straight into file pages
   uint64_t host_checksum_bytes = 0;  // device-tier bytes hashed by host workers (rest: FNV kernels)
   uint64_t helper_bytes = 0;         // image bytes D2H'd by helper GPUs' copy engines (NVLink read)
+  uint64_t direct_io_bytes = 0;      // fixed-region bytes written O_DIRECT (flush_mmap = 2)
   float pack_ms = 0, d2h_ms = 0;
   uint32_t kernel_launches = 0, copies = 0;
   cudaEvent_t ev_start = nullptr, ev_capture = nullptr, ev_d2h_first = nullptr,

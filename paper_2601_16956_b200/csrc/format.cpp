@@ -188,7 +188,14 @@ file_writer::file_writer(const std::string& path, uint64_t tre, uint64_t plan_ha
 
 file_writer::~file_writer() {
   if (map_) ::munmap(map_, tre_);
+  if (dfd_ >= 0) ::close(dfd_);
   if (fd_ >= 0) ::close(fd_);
+}
+
+bool file_writer::open_direct() {
+  if (!io_ || dfd_ >= 0 || map_) return dfd_ >= 0;
+  dfd_ = ::open(path_.c_str(), O_WRONLY | O_DIRECT);
+  return dfd_ >= 0;
 }
 
 void file_writer::release_mapping() {
@@ -221,8 +228,29 @@ void file_writer::populate(uint64_t off, uint64_t n) {
 void file_writer::write_fixed(uint64_t off, const void* p, size_t n) {
   if (!io_ || n == 0) return;
   if (off < header_reserved || off + n > tre_) fail(TS_ERR_IO, "fixed write outside the tensor region");
-  if (map_) std::memcpy(map_ + off, p, n);
-  else pwrite_all(fd_, static_cast<const uint8_t*>(p), n, off, path_);
+  if (map_) {
+    std::memcpy(map_ + off, p, n);
+    return;
+  }
+  const auto* b = static_cast<const uint8_t*>(p);
+  constexpr uint64_t blk = 4096;
+  // O_DIRECT needs file offset, length and buffer aligned: only when the
+  // buffer and the file offset share their offset within a block
+  if (dfd_ >= 0 && ((reinterpret_cast<uintptr_t>(b) - off) & (blk - 1)) == 0) {
+    const uint64_t a = (off + blk - 1) & ~(blk - 1), e = (off + n) & ~(blk - 1);
+    if (e > a) {
+      if (a > off) pwrite_all(fd_, b, a - off, off, path_);
+      const ssize_t k = ::pwrite(dfd_, b + (a - off), e - a, static_cast<off_t>(a));
+      if (k == static_cast<ssize_t>(e - a)) {
+        direct_bytes_ += e - a;
+        if (off + n > e) pwrite_all(fd_, b + (e - off), off + n - e, e, path_);
+        return;
+      }
+      // short or refused direct write: finish the whole range buffered
+      // (the bytes are all in the window; rewriting them is idempotent)
+    }
+  }
+  pwrite_all(fd_, b, n, off, path_);
 }
 
 void file_writer::write_at(uint64_t off, const void* p, size_t n) {

@@ -8,6 +8,7 @@
 //   MANIFEST.tlv                   format.cpp:292-405
 #pragma once
 
+#include <atomic>
 #include <functional>
 #include <string>
 #include <vector>
@@ -71,6 +72,15 @@ class file_writer {
   // parallel, so many flush threads can fill one file concurrently.
   void map_fixed_region();
   bool mapped() const { return map_ != nullptr; }
+  // Kernel-bypass fixed-region writes (the reference's flush path with the
+  // page cache taken out): a second descriptor opened O_DIRECT;
+  // write_fixed sends the 4 KiB-aligned body of a write through it straight
+  // from the pinned staging window (DMA from the pool, no page-cache copy)
+  // and only the ragged head/tail through pwrite(2). Returns false (positional
+  // buffered writes stay) where the filesystem refuses O_DIRECT (tmpfs).
+  bool open_direct();
+  bool direct() const { return dfd_ >= 0; }
+  uint64_t direct_bytes() const { return direct_bytes_.load(); }
   // Pre-faults [off, off+n) of the mapping (MADV_POPULATE_WRITE): page
   // allocation for the file overlaps the device-side capture and D2H.
   void populate(uint64_t off, uint64_t n);
@@ -85,6 +95,8 @@ class file_writer {
  private:
   std::string path_;
   int fd_ = -1;
+  int dfd_ = -1;
+  std::atomic<uint64_t> direct_bytes_{0};  // (flush threads of one file write concurrently)
   uint64_t tre_;
   bool io_;
   bool reused_ = false;

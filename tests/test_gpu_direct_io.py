@@ -1,0 +1,89 @@
+"""O_DIRECT flushes (EngineConfig.flush_mmap = 2, SURVEY §8 f2 "kernel-bypass
+flush"): each staged window's 4 KiB-aligned body goes from the pinned pool to
+the file with O_DIRECT (no page-cache copy), the ragged head/tail with
+pwrite(2). The files must equal the oracle's canonical checkpoint byte for
+byte and restore bit-exactly; on a filesystem that refuses O_DIRECT (tmpfs)
+the writer stays buffered and the result is the same."""
+import os
+import random
+import shutil
+
+import pytest
+
+from conftest import read_tree
+from gpu_helpers import checkpoint_recipe
+from paper_2601_16956_b200 import api
+from test_gpu_fuzz import random_recipe
+
+pytestmark = pytest.mark.gpu
+
+
+def direct_dir(tmp_path):
+    """A scratch directory on a filesystem that accepts O_DIRECT, or None."""
+    root = os.environ.get("GRAFT_REPO_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for d in (str(tmp_path), "/var/tmp", os.path.join(root, "gpurun_out")):
+        try:
+            os.makedirs(d, exist_ok=True)
+            probe = os.path.join(d, ".odirect_probe_%d" % os.getpid())
+            fd = os.open(probe, os.O_WRONLY | os.O_CREAT | os.O_DIRECT, 0o644)
+            os.close(fd)
+            os.unlink(probe)
+            return os.path.join(d, "odirect_%d" % os.getpid())
+        except OSError:
+            continue
+    return None
+
+
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("mode", ["ring", "direct"])
+def test_direct_io_parity(gpu, oracle, tmp_path, seed, mode):
+    base = direct_dir(tmp_path) or str(tmp_path / "buffered")
+    try:
+        rng = random.Random(7000 + seed)
+        rec = random_recipe(rng)
+        w = rng.choice([4096, 65536, 1 << 20])
+        cfg = api.EngineConfig(d2h_mode=mode, raw_chunk_bytes=w, staging_capacity_bytes=8 << 20,
+                               device_staging_bytes=1 << 24, flush_workers=rng.choice([1, 3]), flush_mmap=2)
+        ours = os.path.join(base, "ours")
+        checkpoint_recipe(rec, ours, cfg)
+        ref = str(tmp_path / "oracle")
+        orec = oracle.load_recipe_text(rec.to_text())
+        oracle.write_checkpoint(orec, ref, ser_chunk=min(cfg.serialized_chunk_bytes, cfg.staging_capacity_bytes))
+        assert read_tree(ours) == read_tree(ref), (seed, mode)
+        for rs, spec in zip(api.restore_checkpoint(os.path.join(ours, "MANIFEST.tlv")), rec.ranks):
+            for o, so in zip(rs.objects, spec.objects):
+                if o.is_raw():
+                    got = o.payload.cpu().numpy() if o.payload.is_cuda else o.payload.numpy()
+                    exp = oracle.fill_pattern(so.size, spec.seed, so.space, rec.pit, so.offset)
+                    assert (got == exp).all(), (seed, o.object_id)
+    finally:
+        shutil.rmtree(base, ignore_errors=True)
+
+
+def test_direct_io_engages(gpu, tmp_path):
+    """On an O_DIRECT-capable filesystem the aligned bodies of the windows take
+    the O_DIRECT path (ticket stat direct_io_bytes); the files are checked by
+    a restore."""
+    import torch
+
+    base = direct_dir(tmp_path)
+    if base is None:
+        pytest.skip("no O_DIRECT-capable filesystem on this box")
+    try:
+        n = 24 << 20
+        x = torch.arange(n // 4, dtype=torch.int32, device="cuda")
+        eng = api.CheckpointEngine(api.EngineConfig(raw_chunk_bytes=1 << 20, staging_capacity_bytes=16 << 20,
+                                                    device_staging_bytes=64 << 20, flush_mmap=2), 0, 0)
+        sess = api.CheckpointSession(os.path.join(base, "c"), 1, 1, None, n_ranks=1)
+        st = api.RankState(objects=[api.StateObject(1, size_bytes=n, payload=x)])
+        t = eng.issue_checkpoint(sess, st, 1)
+        eng.pre_update_barrier(t)
+        t.wait_persisted()
+        sess.wait_complete(60)
+        s = t.stats()
+        assert s["direct_io_bytes"] >= n - (2 << 20), s
+        rs = api.restore_checkpoint(os.path.join(base, "c", "MANIFEST.tlv"))
+        assert torch.equal(rs[0].objects[0].payload.cuda().view(torch.int32).view(-1), x)
+        eng.shutdown()
+    finally:
+        shutil.rmtree(base, ignore_errors=True)
