@@ -46,7 +46,7 @@ def random_cfg(rng):
     return api.EngineConfig(
         d2h_mode=mode, raw_chunk_bytes=w, staging_capacity_bytes=rng.choice([w, 2 * w + 7, 8 << 20]),
         device_staging_bytes=rng.choice([8192, 1 << 16, 1 << 24]), flush_workers=rng.choice([1, 2, 5]),
-        checksum_on_gpu=rng.random() < 0.7, flush_mmap=rng.random() < 0.7,
+        checksum_on_gpu=rng.random() < 0.7, flush_mmap=rng.choice([0, 1, 1, 2]),
         pack_kernel=rng.choice(["warp", "bulk"]), bulk_min_bytes=32768,
         serialized_chunk_bytes=rng.choice([1 << 20, 1 << 20, 4096]))
 
