@@ -87,3 +87,42 @@ def test_direct_io_engages(gpu, tmp_path):
         eng.shutdown()
     finally:
         shutil.rmtree(base, ignore_errors=True)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_direct_io_recycled_files(gpu, oracle, tmp_path, seed):
+    """Rotation on a disk filesystem with O_DIRECT flushes: checkpoint A's files
+    are retired into the spare directory and taken over (renamed, re-sized,
+    every byte rewritten) by checkpoint B of the same layout and other bytes;
+    B's tree must equal the oracle's."""
+    base = direct_dir(tmp_path) or str(tmp_path / "buffered")
+    try:
+        # same layout (same file names: every file is recycled), other bytes
+        ra, rb = random_recipe(random.Random(9100 + seed)), random_recipe(random.Random(9100 + seed))
+        for r in rb.ranks:
+            r.seed = (r.seed + 1) % 2**64
+        spare = os.path.join(base, ".spare")
+        cfg = api.EngineConfig(raw_chunk_bytes=65536, staging_capacity_bytes=8 << 20, device_staging_bytes=1 << 24,
+                               flush_mmap=2)
+        for rec, name in ((ra, "a"), (rb, "b")):
+            if name == "b":
+                api.retire_checkpoint(os.path.join(base, "a"), spare)
+                n_spares = len(os.listdir(spare))
+            session = api.CheckpointSession(os.path.join(base, name), rec.ckpt_id, rec.iteration,
+                                            rec.manifest_echo(), n_ranks=len(rec.ranks))
+            states = [api.materialize_payloads(r, 0, rec.pit) for r in rec.ranks]
+            engines = [api.CheckpointEngine(cfg, r.rank_id, 0) for r in rec.ranks]
+            for e in engines:
+                e.set_spare_dir(spare)
+            for t in [e.issue_checkpoint(session, s, rec.iteration) for e, s in zip(engines, states)]:
+                t.wait_persisted()
+            session.wait_complete(120)
+            for e in engines:
+                e.shutdown()
+        ref = str(tmp_path / "oracle")
+        oracle.write_checkpoint(oracle.load_recipe_text(rb.to_text()), ref,
+                                ser_chunk=min(cfg.serialized_chunk_bytes, cfg.staging_capacity_bytes))
+        assert read_tree(os.path.join(base, "b")) == read_tree(ref), seed
+        assert n_spares > 0 and len(os.listdir(spare)) < n_spares  # B took A's files over
+    finally:
+        shutil.rmtree(base, ignore_errors=True)
