@@ -334,10 +334,15 @@ typedef struct ts_restore_stats {
   uint32_t kernel_launches;
   uint32_t _pad;
   uint64_t direct_bytes; /* fixed-region bytes copied H2D straight from page-locked files (no pread) */
+  uint64_t direct_io_bytes; /* fixed-region bytes read O_DIRECT (ts_restore_set_direct_io) */
 } ts_restore_stats;
 /* 1 (default): files page-locked by this process (file_dma rotation) are read
  * by the copy engines from their page cache; 0: always pread into pinned memory. */
 ts_status ts_restore_set_file_cache(ts_restore* r, int use);
+/* 1: fixed-region reads of files that are not page-locked go O_DIRECT from the
+ * disk into the pinned windows (4 KiB-aligned bodies; ragged ends and
+ * filesystems that refuse O_DIRECT, e.g. tmpfs, use pread). 0 (default): pread. */
+ts_status ts_restore_set_direct_io(ts_restore* r, int use);
 ts_status ts_restore_rank(ts_restore* r, int index, const ts_object_desc* dst, size_t n,
                           int device, void* stream, ts_restore_stats* stats);
 ts_status ts_restore_structured(ts_restore* r, int index, uint64_t object_id, ts_value** out);

@@ -135,7 +135,7 @@ class RestoreStats(C.Structure):
     _fields_ = [("bytes", C.c_uint64), ("read_s", C.c_double), ("verify_s", C.c_double),
                 ("h2d_unpack_s", C.c_double), ("total_s", C.c_double), ("unpack_ms", C.c_float),
                 ("h2d_ms", C.c_float), ("kernel_launches", C.c_uint32), ("_pad", C.c_uint32),
-                ("direct_bytes", C.c_uint64)]
+                ("direct_bytes", C.c_uint64), ("direct_io_bytes", C.c_uint64)]
 
 
 class VerifyIssue(C.Structure):
@@ -196,6 +196,7 @@ _sig("ts_engine_numa_node", i32, P)
 _sig("ts_engine_provision_spares", i32, P, C.c_char_p, C.POINTER(RankInfo), C.POINTER(ObjectDesc), C.c_size_t,
      i32, C.POINTER(C.c_uint64))
 _sig("ts_restore_set_file_cache", i32, P, i32)
+_sig("ts_restore_set_direct_io", i32, P, i32)
 _sig("ts_file_cache_bytes", C.c_uint64)
 _sig("ts_file_cache_release_all", i32, C.POINTER(C.c_uint64))
 _sig("ts_session_create", i32, C.c_char_p, u64, u64, C.POINTER(ManifestEcho), i32, i32, C.POINTER(P))

@@ -391,6 +391,10 @@ ts_status ts_restore_set_file_cache(ts_restore* r, int use) {
   return guard([&] { r->r->use_file_cache = use != 0; });
 }
 
+ts_status ts_restore_set_direct_io(ts_restore* r, int use) {
+  return guard([&] { r->r->direct_io = use != 0; });
+}
+
 ts_status ts_restore_open(const char* manifest_path, ts_restore** out) {
   return guard([&] {
     auto* h = new ts_restore;

@@ -5,6 +5,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <unordered_map>
@@ -24,10 +25,33 @@ void rtrace(const char* what, int64_t t0) {
 
 struct fd_holder {
   int fd = -1;
+  int dfd = -1;  // O_DIRECT descriptor (restore_handle::direct_io), else -1
   ~fd_holder() {
+    if (dfd >= 0) ::close(dfd);
     if (fd >= 0) ::close(fd);
   }
 };
+
+// Reads [off, off+n) of a file into p: the 4 KiB-aligned body O_DIRECT when
+// the descriptor exists and p and off share their offset within a block, the
+// rest (and any refused or short direct read) with pread.
+void read_range(const fd_holder& f, uint8_t* p, uint64_t n, uint64_t off, const std::string& path,
+                std::atomic<uint64_t>* direct) {
+  constexpr uint64_t blk = 4096;
+  if (f.dfd >= 0 && ((reinterpret_cast<uintptr_t>(p) - off) & (blk - 1)) == 0) {
+    const uint64_t a = (off + blk - 1) & ~(blk - 1), e = (off + n) & ~(blk - 1);
+    if (e > a) {
+      const ssize_t k = ::pread(f.dfd, p + (a - off), e - a, static_cast<off_t>(a));
+      if (k == static_cast<ssize_t>(e - a)) {
+        *direct += e - a;
+        if (a > off) pread_all(f.fd, p, a - off, off, path);
+        if (off + n > e) pread_all(f.fd, p + (e - off), off + n - e, e, path);
+        return;
+      }
+    }
+  }
+  pread_all(f.fd, p, n, off, path);
+}
 
 // Process-wide staging reused across restores (pinning is slow; allocate once).
 std::mutex g_stage_mu;
@@ -296,6 +320,7 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
   for (size_t k = 0; k < rc.files.size(); ++k) {
     fds[k].fd = ::open(rc.files[k].path.c_str(), O_RDONLY);
     if (fds[k].fd < 0) fail(TS_ERR_MISSING_FILE, "cannot open " + rc.files[k].path);
+    if (direct_io) fds[k].dfd = ::open(rc.files[k].path.c_str(), O_RDONLY | O_DIRECT);  // -1: pread
   }
   // Page-locked files (registered by this process's engines): H2D straight
   // from the page cache, no pread. Pinned against claims/drops until the end.
@@ -310,6 +335,7 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
   regs.map.assign(rc.files.size(), nullptr);
   regs.key.resize(rc.files.size());
   uint64_t direct_bytes = 0;
+  std::atomic<uint64_t> odirect_bytes{0};
   if (use_file_cache)
     for (size_t k = 0; k < rc.files.size(); ++k)
       if (file_img[k].second > 0) {
@@ -465,7 +491,8 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
         const uint64_t x = std::get<1>(rd), y = std::get<2>(rd);
         pool.submit([&, ws, k, x, y, lo, hi, slot, hs, direct] {
           try {
-            pread_all(fds[k].fd, hs + (x - lo), y - x, header_reserved + (x - file_img[k].first), rc.files[k].path);
+            read_range(fds[k], hs + (x - lo), y - x, header_reserved + (x - file_img[k].first), rc.files[k].path,
+                       &odirect_bytes);
           } catch (const error& e) {
             set_err(e);
           }
@@ -569,6 +596,7 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
     stats->h2d_unpack_s = h2d_ms * 1e-3;
     stats->h2d_ms = h2d_ms;
     stats->direct_bytes = direct_bytes;
+    stats->direct_io_bytes = odirect_bytes.load();
     stats->unpack_ms = unpack_ms;
     stats->total_s = (now_ns() - t_begin) * 1e-9;
     stats->kernel_launches = launches;

@@ -84,6 +84,11 @@ def test_direct_io_engages(gpu, tmp_path):
         assert s["direct_io_bytes"] >= n - (2 << 20), s
         rs = api.restore_checkpoint(os.path.join(base, "c", "MANIFEST.tlv"))
         assert torch.equal(rs[0].objects[0].payload.cuda().view(torch.int32).view(-1), x)
+        # and read back O_DIRECT
+        r = api.Restorer(os.path.join(base, "c", "MANIFEST.tlv"), direct_io=True)
+        rs = r.restore_rank(0)
+        assert r.last_stats["direct_io_bytes"] >= n - (2 << 20), r.last_stats
+        assert torch.equal(rs.objects[0].payload.cuda().view(torch.int32).view(-1), x)
         eng.shutdown()
     finally:
         shutil.rmtree(base, ignore_errors=True)
@@ -124,5 +129,31 @@ def test_direct_io_recycled_files(gpu, oracle, tmp_path, seed):
                                 ser_chunk=min(cfg.serialized_chunk_bytes, cfg.staging_capacity_bytes))
         assert read_tree(os.path.join(base, "b")) == read_tree(ref), seed
         assert n_spares > 0 and len(os.listdir(spare)) < n_spares  # B took A's files over
+    finally:
+        shutil.rmtree(base, ignore_errors=True)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_direct_io_restore(gpu, oracle, tmp_path, seed):
+    """Restore with O_DIRECT reads (Restorer(direct_io=True)) of a checkpoint on
+    a disk filesystem: bit-exact shards, same result as the pread path."""
+    base = direct_dir(tmp_path) or str(tmp_path / "buffered")
+    try:
+        rng = random.Random(9300 + seed)
+        rec = random_recipe(rng)
+        cfg = api.EngineConfig(raw_chunk_bytes=rng.choice([4096, 65536, 1 << 20]), staging_capacity_bytes=8 << 20,
+                               device_staging_bytes=1 << 24, flush_mmap=rng.choice([1, 2]))
+        ours = os.path.join(base, "ours")
+        checkpoint_recipe(rec, ours, cfg)
+        os.sync()
+        r = api.Restorer(os.path.join(ours, "MANIFEST.tlv"), direct_io=True)
+        for i, spec in enumerate(rec.ranks):
+            rs = r.restore_rank(i)
+            assert rs.rank_id == spec.rank_id
+            for o, so in zip(rs.objects, spec.objects):
+                if o.is_raw():
+                    got = o.payload.cpu().numpy() if o.payload.is_cuda else o.payload.numpy()
+                    exp = oracle.fill_pattern(so.size, spec.seed, so.space, rec.pit, so.offset)
+                    assert (got == exp).all(), (seed, o.object_id)
     finally:
         shutil.rmtree(base, ignore_errors=True)
