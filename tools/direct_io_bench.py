@@ -18,6 +18,16 @@ import torch  # noqa: E402
 from paper_2601_16956_b200 import api  # noqa: E402
 
 
+def drop_caches() -> bool:
+    os.sync()
+    try:
+        with open("/proc/sys/vm/drop_caches", "w") as f:
+            f.write("3\n")
+        return True
+    except OSError:
+        return False
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gb", type=float, default=8.0)
@@ -27,6 +37,8 @@ def main():
     ap.add_argument("--modes", default="1,2")
     ap.add_argument("--workers", type=int, default=0, help="flush workers (0: engine default)")
     ap.add_argument("--window-mb", type=int, default=0, help="D2H window MiB (0: engine default)")
+    ap.add_argument("--restore", action="store_true",
+                    help="also time cold restores (caches dropped) with pread and with O_DIRECT reads")
     a = ap.parse_args()
     per = int(a.gb * 1e9 / a.objects) // 4096 * 4096
     objs = [api.StateObject(i + 1, file_id=i % 4, size_bytes=per,
@@ -62,6 +74,21 @@ def main():
                               "direct_io_frac": round(s["direct_io_bytes"] / total, 3),
                               "workers": cfg.flush_workers, "window_mb": cfg.raw_chunk_bytes >> 20}), flush=True)
             eng.shutdown()
+            if a.restore:
+                for dio in (False, True, False, True):
+                    dropped = drop_caches()
+                    r = api.Restorer(os.path.join(d, "MANIFEST.tlv"), direct_io=dio)
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    rs = r.restore_rank(0)
+                    torch.cuda.synchronize()
+                    dt = time.perf_counter() - t0
+                    ok = all(torch.equal(o.payload, so.payload) for o, so in zip(rs.objects, objs))
+                    print(json.dumps({"restore": "O_DIRECT" if dio else "pread", "written_by": mode,
+                                      "caches_dropped": dropped, "gbps": round(total / dt / 1e9, 2),
+                                      "direct_io_frac": round(r.last_stats["direct_io_bytes"] / total, 3),
+                                      "bit_exact": ok}), flush=True)
+                    del rs, r
             shutil.rmtree(d, ignore_errors=True)
             os.sync()
 
