@@ -341,7 +341,8 @@ typedef struct ts_restore_stats {
 ts_status ts_restore_set_file_cache(ts_restore* r, int use);
 /* 1: fixed-region reads of files that are not page-locked go O_DIRECT from the
  * disk into the pinned windows (4 KiB-aligned bodies; ragged ends and
- * filesystems that refuse O_DIRECT, e.g. tmpfs, use pread). 0 (default): pread. */
+ * filesystems that refuse O_DIRECT, e.g. tmpfs, use pread). 0: pread.
+ * -1 (default): O_DIRECT for files mostly absent from the page cache (cold). */
 ts_status ts_restore_set_direct_io(ts_restore* r, int use);
 ts_status ts_restore_rank(ts_restore* r, int index, const ts_object_desc* dst, size_t n,
                           int device, void* stream, ts_restore_stats* stats);

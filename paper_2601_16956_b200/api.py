@@ -694,16 +694,17 @@ class Restorer:
     """restore_checkpoint split per rank: open the manifest, list a rank's
     objects, restore it into caller-provided (or freshly allocated) shards."""
 
-    def __init__(self, manifest_path: str, use_file_cache: bool = True, direct_io: bool = False):
+    def __init__(self, manifest_path: str, use_file_cache: bool = True, direct_io: Optional[bool] = None):
         """`use_file_cache`: read files this process page-locked (file_dma
         rotation) straight from their page cache; False: always pread.
-        `direct_io`: other files' fixed regions are read O_DIRECT (disks)."""
+        `direct_io`: other files' fixed regions are read O_DIRECT (disks);
+        None (default): only files mostly absent from the page cache."""
         h = C.c_void_p()
         N.call(N.lib.ts_restore_open, manifest_path.encode(), C.byref(h))
         self.h = h.value
         self.last_stats: Dict[str, Any] = {}
         N.call(N.lib.ts_restore_set_file_cache, self.h, int(use_file_cache))
-        N.call(N.lib.ts_restore_set_direct_io, self.h, int(direct_io))
+        N.call(N.lib.ts_restore_set_direct_io, self.h, -1 if direct_io is None else int(direct_io))
 
     def __del__(self, _close=N.lib.ts_restore_close):
         h, self.h = getattr(self, "h", None), None

@@ -392,7 +392,7 @@ ts_status ts_restore_set_file_cache(ts_restore* r, int use) {
 }
 
 ts_status ts_restore_set_direct_io(ts_restore* r, int use) {
-  return guard([&] { r->r->direct_io = use != 0; });
+  return guard([&] { r->r->direct_io = use < 0 ? -1 : use != 0; });
 }
 
 ts_status ts_restore_open(const char* manifest_path, ts_restore** out) {

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <sys/mman.h>
 #include <cstdio>
 #include <cstdlib>
 #include <unordered_map>
@@ -31,6 +32,25 @@ struct fd_holder {
     if (fd >= 0) ::close(fd);
   }
 };
+
+// True when fewer than half of 64 sampled pages of [0, len) are in the page
+// cache (mincore over a read-only mapping): a cold file on a disk, where
+// O_DIRECT reads beat pread (measured 3.8-4.0 vs 1.6-2.8 GB/s); warm files
+// (just written) stay on pread from the page cache.
+bool mostly_uncached(int fd, uint64_t len) {
+  if (len < (8ull << 20)) return false;
+  void* m = ::mmap(nullptr, len, PROT_READ, MAP_SHARED, fd, 0);
+  if (m == MAP_FAILED) return false;
+  const uint64_t pg = 4096, pages = len / pg;
+  int resident = 0;
+  for (int i = 0; i < 64; ++i) {
+    unsigned char v = 0;
+    const uint64_t at = (pages * static_cast<uint64_t>(2 * i + 1) / 128) * pg;
+    if (::mincore(static_cast<uint8_t*>(m) + at, pg, &v) == 0 && (v & 1)) ++resident;
+  }
+  ::munmap(m, len);
+  return resident < 32;
+}
 
 // Reads [off, off+n) of a file into p: the 4 KiB-aligned body O_DIRECT when
 // the descriptor exists and p and off share their offset within a block, the
@@ -320,7 +340,8 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
   for (size_t k = 0; k < rc.files.size(); ++k) {
     fds[k].fd = ::open(rc.files[k].path.c_str(), O_RDONLY);
     if (fds[k].fd < 0) fail(TS_ERR_MISSING_FILE, "cannot open " + rc.files[k].path);
-    if (direct_io) fds[k].dfd = ::open(rc.files[k].path.c_str(), O_RDONLY | O_DIRECT);  // -1: pread
+    if (direct_io > 0 || (direct_io < 0 && mostly_uncached(fds[k].fd, rc.files[k].region_end)))
+      fds[k].dfd = ::open(rc.files[k].path.c_str(), O_RDONLY | O_DIRECT);  // -1 (tmpfs): pread
   }
   // Page-locked files (registered by this process's engines): H2D straight
   // from the page cache, no pread. Pinned against claims/drops until the end.

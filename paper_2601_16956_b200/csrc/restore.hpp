@@ -31,8 +31,9 @@ struct restore_handle {
   // Files page-locked by this process (file_dma rotation) are read by the copy
   // engines straight from their page cache instead of pread into pinned memory.
   bool use_file_cache = true;
-  // Cold reads from disk: O_DIRECT into the pinned windows (page cache bypassed).
-  bool direct_io = false;
+  // Reads from disk O_DIRECT into the pinned windows (page cache bypassed):
+  // 1 always, 0 never, -1 (default) for files mostly not in the page cache.
+  int direct_io = -1;
 
   explicit restore_handle(const std::string& manifest_path);
   void load_rank(int index);

@@ -75,8 +75,8 @@ def main():
                               "workers": cfg.flush_workers, "window_mb": cfg.raw_chunk_bytes >> 20}), flush=True)
             eng.shutdown()
             if a.restore:
-                for dio in (False, True, False, True):
-                    dropped = drop_caches()
+                for dio, cold in ((False, True), (True, True), (None, True), (None, False)):
+                    dropped = drop_caches() if cold else False
                     r = api.Restorer(os.path.join(d, "MANIFEST.tlv"), direct_io=dio)
                     torch.cuda.synchronize()
                     t0 = time.perf_counter()
@@ -84,7 +84,8 @@ def main():
                     torch.cuda.synchronize()
                     dt = time.perf_counter() - t0
                     ok = all(torch.equal(o.payload, so.payload) for o, so in zip(rs.objects, objs))
-                    print(json.dumps({"restore": "O_DIRECT" if dio else "pread", "written_by": mode,
+                    print(json.dumps({"restore": {False: "pread", True: "O_DIRECT", None: "auto"}[dio],
+                                      "written_by": mode,
                                       "caches_dropped": dropped, "gbps": round(total / dt / 1e9, 2),
                                       "direct_io_frac": round(r.last_stats["direct_io_bytes"] / total, 3),
                                       "bit_exact": ok}), flush=True)
