@@ -30,7 +30,6 @@ sys.path.insert(0, ROOT)
 
 # BASELINE.json's metric; `value` is the box GB/s, the blocked ms are in "blocked"
 METRIC = "checkpoint GB/s per GPU & box (1/2/4/8 B200); training blocked ms/ckpt"
-PCIE_D2H_MEASURED_GBPS = 57.2  # pinned cudaMemcpy D2H on this pool's B200 (gpurun_out/probe_box.json)
 
 
 def peaks():
@@ -103,6 +102,26 @@ def ncu_traffic(cfg: str, mode: str, pack_kernel: str):
     return int(t["traffic_bytes_per_launch"])
 
 
+def pcie_d2h_peak(dev) -> float:
+    """Pinned D2H copy-engine rate of this GPU, measured in the same run (the
+    D2H roofline): best of 3 x 2 GiB cudaMemcpyAsync into page-locked memory."""
+    import torch
+
+    n = 2 << 30
+    src = torch.empty(n, dtype=torch.uint8, device=dev)
+    dst = torch.empty(n, dtype=torch.uint8).pin_memory()
+    best = 0.0
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dst.copy_(src, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = max(best, n / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    del src, dst
+    return best
+
+
 def host_mem_avail() -> int:
     try:
         with open("/proc/meminfo") as f:
@@ -121,83 +140,142 @@ def dist_info():
     return ws, rank, local
 
 
-def sample_recipe(cfg: str, rank: int, max_raw: int = 8):
-    """Bounded sample of the workload for the CPU reference: the first `max_raw`
-    raw objects of this rank (+ its metadata), same sizes and patterns."""
+def workload_config(cfg: str, spec) -> dict:
+    """The `config` object of both arms (ours and --impl reference): the named
+    BASELINE.json workload; engine knobs go under "engine" in our line."""
+    names = {"cfg1": "GPT-2 small generate_layout, 1 rank", "cfg1b": "GPT-2 small fp32 + Adam, 1 rank",
+             "cfg2": "Llama-2 7B ZeRO-1 x8, rank-r shard", "cfg3": "Llama-2 13B ZeRO-3 x8, rank-r shard",
+             "cfg4": "Llama-2 70B ZeRO-3 x8, rank-r shard (14 B/param)"}
+    return {"workload": f"{cfg}: {names.get(cfg, cfg)}, {len(spec.objects)} objects, "
+                        f"{spec.raw_bytes / 1e9:.3f} GB/rank",
+            "l2": "inputs > L2 (126 MB)"}
+
+
+def sample_recipe(cfg: str, rank: int, max_bytes: int):
+    """Bounded sample of rank `rank`'s shard for the CPU reference: its raw
+    objects in rank order until `max_bytes` (at least one; the whole rank when
+    it fits), plus its metadata object. Same sizes and patterns as the full
+    workload."""
     from paper_2601_16956_b200 import synthetic as S
 
     rec = S.config_recipe(cfg, rank)
     r = rec.ranks[0]
-    raws = [o for o in r.objects if o.kind == 0][:max_raw]
-    metas = [o for o in r.objects if o.kind == 1 and o.meta[0] == "meta"]
-    r.objects = raws + metas
-    return rec
+    raws, acc = [], 0
+    for o in (o for o in r.objects if o.kind == 0):
+        if raws and acc + o.size > max_bytes:
+            break
+        raws.append(o)
+        acc += o.size
+    whole = len(raws) == len([o for o in r.objects if o.kind == 0])
+    metas = [o for o in r.objects if o.kind == 1 and (whole or o.meta[0] == "meta")]
+    r.objects = [o for o in r.objects if (o.kind == 0 and o in raws) or o in metas]
+    return rec, whole
 
 
-def run_reference(args, sample_max_raw=None, steps=None, warmup=None):
-    """The reference CPU implementation (oracle/_ref/ts_ref_driver, built from
-    /root/reference) on a bounded sample of this config, one process, its default
-    flush workers on every other host core + its 1 copier thread, files to /dev/shm."""
+REF_RATE_GUESS = 0.8e9  # B/s per reference process (FNV under its monitor; BASELINE.md §2, r1 box runs)
+
+
+def run_reference(cfg: str, n: int, steps: int, warmup: int, budget_s: float):
+    """The compiled reference (oracle/_ref/ts_ref_driver, built unmodified from
+    /root/reference) as N independent OS processes, one per rank (BASELINE.md
+    §3: never ranks as threads of one process), each pinned to its own disjoint
+    set of host cores with its flush workers on all but one of them, each
+    checkpointing a bounded sample of ITS rank's shard (`budget_s` of work for
+    the whole run at the reference's rate), files on /dev/shm, one restore after
+    the last step. Returns None when the driver is not built."""
     drv = os.path.join(ROOT, "oracle", "_ref", "ts_ref_driver")
     if not os.path.exists(drv):
         return None
-    from paper_2601_16956_b200 import synthetic as S
-
-    if sample_max_raw is None:  # the whole rank when it is small (cfg1), else a ~3 GB sample
-        full = S.config_recipe(args.config, 0).ranks[0]
-        sample_max_raw = len(full.objects) if full.raw_bytes <= (4 << 30) else 8
-    rec = sample_recipe(args.config, 0, sample_max_raw)
-    whole = len([o for o in rec.ranks[0].objects if o.kind == 0]) == len(
-        [o for o in S.config_recipe(args.config, 0).ranks[0].objects if o.kind == 0])
-    sample_bytes = rec.ranks[0].raw_bytes
+    cores = sorted(os.sched_getaffinity(0))
+    per = max(1, len(cores) // n)
+    sets = [cores[i * per:(i + 1) * per] or cores[:1] for i in range(n)]
+    reps = warmup + steps + 2  # (+ the restore, ~half the snapshot rate)
+    want = int(budget_s / reps * REF_RATE_GUESS * (1.0 if per >= 4 else per / 4))
+    avail = host_mem_avail()
+    if avail:  # payload + staging cache + tmpfs files per process
+        want = min(want, int(0.6 * avail / n / 3))
     tmp = tempfile.mkdtemp(dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
+    procs, meta = [], []
     try:
-        rp = os.path.join(tmp, "sample.recipe")
-        with open(rp, "w") as f:
-            f.write(rec.to_text())
-        cap = 1 << (max(sample_bytes, 256 << 20) - 1).bit_length()
-        workers = max(4, (os.cpu_count() or 8) - 1)  # all the host threads it can use
-        cmd = [drv, "bench", rp, os.path.join(tmp, "ckpt"), "--workers", str(workers), "--cache", str(cap),
-               "--reps", str(steps if steps is not None else 1), "--warmup",
-               str(warmup if warmup is not None else 0), "--restore"]
-        out = subprocess.run(cmd, capture_output=True, text=True, check=True).stdout
-        rows = [json.loads(l) for l in out.splitlines() if l.startswith("{")]
+        for r in range(n):
+            rec, whole = sample_recipe(cfg, r, want)
+            b = rec.ranks[0].raw_bytes
+            rp = os.path.join(tmp, f"rank{r}.recipe")
+            with open(rp, "w") as f:
+                f.write(rec.to_text())
+            cap = 1 << (max(b, 256 << 20) - 1).bit_length()
+            if avail and n * (2 * b + cap) > 0.8 * avail:
+                cap = 256 << 20  # the reference's default cache (back-pressure)
+            workers = max(1, len(sets[r]) - 1)
+            cmd = ["taskset", "-c", ",".join(map(str, sets[r])), drv, "bench", rp, os.path.join(tmp, f"ckpt{r}"),
+                   "--workers", str(workers), "--cache", str(cap), "--reps", str(steps), "--warmup", str(warmup),
+                   "--restore-last"]
+            if not shutil.which("taskset"):
+                cmd = cmd[3:]
+            procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+            meta.append({"rank": r, "cores": sets[r], "workers": workers, "whole": whole,
+                         "objects": len([o for o in rec.ranks[0].objects if o.kind == 0]), "cache": cap})
+        outs = []
+        for p in procs:
+            out, err = p.communicate()
+            if p.returncode != 0:
+                raise RuntimeError(f"ts_ref_driver failed: {err.strip()[-500:]}")
+            outs.append([json.loads(l) for l in out.splitlines() if l.startswith("{")])
     finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
         shutil.rmtree(tmp, ignore_errors=True)
-    timed = [r for r in rows if not r["warmup"]]
-    snap = sum(r["snapshot_s"] for r in timed)
-    pers = sum(r["persist_s"] for r in timed)
-    b = sum(r["bytes"] for r in timed)
-    rest = [r["restore_s"] for r in timed if r.get("restore_s", -1) > 0]
-    return {"value": b / snap / 1e9, "persist_gbps": b / pers / 1e9, "steps": len(timed),
-            "restore_gbps": round(timed[0]["bytes"] * len(rest) / sum(rest) / 1e9, 4) if rest else None,
-            "bytes_per_step": timed[0]["bytes"], "snapshot_s": [r["snapshot_s"] for r in timed],
-            "issue_ms": [1e3 * r["issue_s"] for r in timed],
-            "sample": f"{args.config} rank 0: first {sample_max_raw} raw objects + metadata "
-                      f"({timed[0]['bytes'] / 1e9:.2f} GB), lazy, {workers} flush workers + 1 copier, files on /dev/shm",
-            "cores": workers + 1, "whole": whole}
+    timed = [[x for x in rows if not x["warmup"]] for rows in outs]
+    bytes_step = [t[0]["bytes"] for t in timed]
+    snap = max(sum(x["snapshot_s"] for x in t) for t in timed)  # slowest rank (box metric)
+    pers = max(sum(x["persist_s"] for x in t) for t in timed)
+    rest = [x["restore_s"] for t in timed for x in t if x.get("restore_s", -1) > 0]
+    k = len(timed[0])
+    whole = all(m["whole"] for m in meta)
+    return {"value": sum(bytes_step) * k / snap / 1e9, "persist_gbps": sum(bytes_step) * k / pers / 1e9,
+            "steps": k, "ms_per_step": 1e3 * snap / k,
+            "restore_gbps": round(sum(bytes_step) / max(rest) / 1e9, 4) if len(rest) == n else None,
+            "bytes_per_step": int(sum(bytes_step)), "bytes_per_step_per_rank": bytes_step,
+            "blocked_ms": 1e3 * max(statistics.mean(x["issue_s"] for x in t) for t in timed),
+            "cores": sum(len(m["cores"]) for m in meta), "whole": whole,
+            "sample": (f"{cfg}: {n} reference process(es), one per rank, each pinned to {per} core(s) "
+                       f"({meta[0]['workers']} flush workers + 1 copier); per rank "
+                       + ("the whole shard" if whole else
+                          f"the first {meta[0]['objects']} raw objects of its shard + its metadata "
+                          f"({bytes_step[0] / 1e9:.2f} GB of the {cfg} shard; the reference's rate is "
+                          f"size-invariant, FNV-bound, BASELINE.md §2-3)")
+                       + "; lazy, files on /dev/shm, restore once after the last step"),
+            "procs": meta}
 
 
 def reference_arm(args):
+    """--impl reference: rank 0 alone (other torchrun ranks exit without work)
+    runs one reference process per GPU of the run."""
     ws, rank, _ = dist_info()
     if rank != 0:
         return
-    r = run_reference(args, steps=args.steps, warmup=args.warmup)
+    n = max(args.gpus, ws)
+    r = run_reference(args.config, n, args.steps, args.warmup, args.ref_budget_s)
     if r is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ts_ref_driver not built"}))
         return
+    from paper_2601_16956_b200 import synthetic as S
+
+    spec = S.config_recipe(args.config, 0).ranks[0]
     line = {"metric": METRIC, "impl": "reference", "value": round(r["value"], 4),
-            "unit": "GB/s", "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
-            "ms_per_step": round(1e3 * statistics.mean(r["snapshot_s"]), 1), "higher_is_better": True,
+            "unit": "GB/s", "n_gpus": n, "steps": r["steps"], "warmup": args.warmup,
+            "ms_per_step": round(r["ms_per_step"], 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": args.config + (" (whole rank)" if r["whole"] else " (bounded CPU sample)"),
-                       "sample": r["sample"]},
+            "config": workload_config(args.config, spec),
+            "sample": r["sample"], "bytes_per_step": r["bytes_per_step"],
             "persist_gbps": round(r["persist_gbps"], 4), "restore_gbps": r["restore_gbps"],
-            "blocked_ms": round(statistics.mean(r["issue_ms"]), 3),
+            "blocked_ms": round(r["blocked_ms"], 3),
             "cpu_baseline": {"value": round(r["value"], 4), "unit": "GB/s", "cores": r["cores"], "kind": "reference",
                              "sample": r["sample"]},
-            "e2e": {"value": round(r["value"], 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+            "e2e": {"value": round(r["persist_gbps"], 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0,
+                    "what": "issue -> files + footers + MANIFEST persisted (wait_persisted), /dev/shm"}}
     print(json.dumps(line))
 
 
@@ -253,7 +331,9 @@ def ours(args):
     # One GPU per rank (NCCL). TS_BENCH_SHARE_GPU=1 runs the N>1 path on fewer
     # GPUs than ranks (gloo, ranks share devices) — a functional check of the
     # multi-rank code path on a 1-GPU box, never a scaling number.
-    share = os.environ.get("TS_BENCH_SHARE_GPU") == "1"
+    local_ws = int(os.environ.get("LOCAL_WORLD_SIZE", str(ws)))
+    share = os.environ.get("TS_BENCH_SHARE_GPU") == "1" or torch.cuda.device_count() < local_ws
+    share_gpu = share
     local_dev = local % torch.cuda.device_count() if share else local
     backend = "gloo" if share else "nccl"
     if ws > 1:
@@ -267,6 +347,7 @@ def ours(args):
 
     rec = S.config_recipe(args.config, rank)
     spec = rec.ranks[0]
+    pcie_peak = pcie_d2h_peak(dev)
     state = api.materialize_payloads(spec, local_dev, 0)
     raw = spec.raw_bytes
     # D2H load balancing: a rank above the mean shard hands part
@@ -519,13 +600,18 @@ def ours(args):
     if args.train_steps > 0:
         blocked = training_phase(args, api, state, spec, cfg, local_dev, dev, it)
 
+    # the TMA bulk kernel runs only for a full device shadow (engine.cpp run_job);
+    # a multi-slot HBM ring (cfg4) packs every chunk with the warp kernel
+    pack_used = "bulk" if (shadow and args.pack_kernel == "bulk") else "warp"
+    pack_label = ("copy-engine DMA" if args.mode == "direct" else
+                  "pack_bulk_kernel (TMA) + pack_kernel" if pack_used == "bulk" else "pack_kernel (warp gather)")
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:  # (N=1 only)
-        r = run_reference(args)
+        r = run_reference(args.config, 1, 3, 1, args.cpu_budget_s)
         if r:
             cpu = {"value": round(r["value"], 4), "unit": "GB/s", "cores": r["cores"], "kind": "reference",
-                   "restore_gbps": r["restore_gbps"],
-                   "sample": r["sample"]}
+                   "persist_gbps": round(r["persist_gbps"], 4), "restore_gbps": r["restore_gbps"],
+                   "bytes_per_step": r["bytes_per_step"], "sample": r["sample"]}
     clocks = clk.summary()
     if rank == 0:
         line = {
@@ -533,27 +619,29 @@ def ours(args):
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(t_ms / args.steps, 2), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {rec.name} rank-r shard, {len(spec.objects)} objects, "
-                                   f"{bytes_step / 1e9:.3f} GB/rank", "d2h_mode": args.mode,
-                       "device_shadow": bool(shadow), "ring_gb": None if shadow else round(ring_bytes / 2**30, 1), "pinned_pool_gb": round(pool / 2**30, 2),
+            "config": workload_config(args.config, spec),
+            "bytes_per_step": int(box_bytes),
+            "engine": {"d2h_mode": args.mode, "device_shadow": bool(shadow),
+                       "ring_gb": None if shadow else round(ring_bytes / 2**30, 1),
+                       "pinned_pool_gb": round(pool / 2**30, 2),
                        "checksums": "host" if args.host_checksum else "gpu", "pack_kernel": args.pack_kernel,
                        "priorities": {"pack": args.pack_priority, "checksums": args.ck_priority},
                        "checksum_host_frac": "auto" if args.ck_host_frac < 0 else args.ck_host_frac,
-                       "numa_node": numa_node, "l2": "inputs > L2 (126 MB)",
+                       "numa_node": numa_node, "shared_gpu": share_gpu,
                        "d2h_helpers": {"devices": list(helpers), "share": round(share, 3)},
                        "step": "update(pattern kernel) + issue + snapshot + checksums (no files)"},
             "per_gpu_gbps": round(value / ws, 3),
             "snapshot_ms_mean": round(statistics.mean(snap_ms), 2),
             "snapshot_gbps_mean": round(bytes_step / (statistics.mean(snap_ms) / 1e3) / 1e9, 3),
             "d2h_gbps": round(image / (statistics.mean(d2h_ms) / 1e3) / 1e9, 3) if min(d2h_ms) > 0 else None,
-            "d2h_frac_pcie": round(image / (statistics.mean(d2h_ms) / 1e3) / 1e9 / PCIE_D2H_MEASURED_GBPS, 3)
+            "d2h_frac_pcie": round(image / (statistics.mean(d2h_ms) / 1e3) / 1e9 / pcie_peak, 3)
             if min(d2h_ms) > 0 else None,
-            "roofline": {"kernel": ("pack_bulk_kernel (TMA) + pack_kernel" if args.pack_kernel == "bulk" else "pack_kernel")
-                         if args.mode != "direct" else "copy-engine DMA",
+            "pcie_d2h_peak_gbps": round(pcie_peak, 2),
+            "roofline": {"kernel": pack_label,
                          "bound": "hbm", "achieved": round(pack_alg / (pack_mean / 1e3) / 1e9, 1),
                          "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(pack_alg / (pack_mean / 1e3) / 1e9 / hbm_peak, 3),
-                         "traffic": ncu_traffic(args.config, args.mode, args.pack_kernel),
+                         "traffic": ncu_traffic(args.config, args.mode, pack_used),
                          "traffic_source": "profiles/ncu_traffic.json (ncu --set full, same workload)",
                          "alg_bytes_per_launch": int(pack_alg),
                          "launch_ms": round(pack_mean, 3)},
@@ -716,7 +804,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg4",
+                    help="BASELINE.json workload: cfg4 (70B ZeRO-3 shard, the north-star config, default), "
+                         "cfg1, cfg1b, cfg2, cfg3")
     ap.add_argument("--mode", default="ring", choices=["ring", "direct", "zerocopy"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--train-steps", type=int, default=3)
@@ -732,7 +822,7 @@ def main():
                     help="share of checksums on host workers (0: all GPU; <0: auto from host rate and cadence)")
     ap.add_argument("--pack-priority", type=int, default=1, help="capture (pack) stream priority (1/0/-1)")
     ap.add_argument("--flush-workers", type=int, default=0, help="host worker threads (default: min(16, cores))")
-    ap.add_argument("--keep", type=int, default=2, help="e2e rotation: checkpoints kept on tmpfs")
+    ap.add_argument("--keep", type=int, default=1, help="e2e rotation: checkpoints kept on tmpfs")
     ap.add_argument("--ckpt-root", default="", help="e2e checkpoint directory root (default /dev/shm)")
     ap.add_argument("--flush-pwrite", action="store_true", help="pool flushes with pwrite(2) instead of mmap copies")
     ap.add_argument("--flush-direct", action="store_true",
@@ -743,6 +833,10 @@ def main():
     ap.add_argument("--fresh-files", action="store_true",
                     help="e2e: new files every checkpoint (no rotation / recycling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=30.0,
+                    help="cpu_baseline: seconds of reference CPU work (bounded sample of the workload)")
+    ap.add_argument("--ref-budget-s", type=float, default=200.0,
+                    help="--impl reference: seconds of reference work for the whole --steps/--warmup run")
     ap.add_argument("--pool-gb", type=float, default=0.0, help="pinned pool cap (default 4 GiB)")
     ap.add_argument("--ring-gb", type=float, default=0.0,
                     help="HBM staging ring when no full device shadow fits (0 = auto: free HBM - 26 GiB)")
@@ -753,8 +847,22 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)
-    else:
-        ours(args)
+        return
+    ws = int(os.environ.get("WORLD_SIZE", "0"))
+    if ws == 0 and args.gpus > 1:
+        # one process per GPU: launch the ranks ourselves (same as the driver's
+        # torchrun command), rank 0 prints the line
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if ws and ws != args.gpus:
+        sys.exit(f"bench: WORLD_SIZE={ws} but --gpus {args.gpus}")
+    ours(args)
 
 
 if __name__ == "__main__":

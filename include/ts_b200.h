@@ -316,7 +316,12 @@ typedef struct ts_restore_object {
 
 /* read_manifest (format.cpp:407-428) */
 ts_status ts_restore_open(const char* manifest_path, ts_restore** out);
+/* Closing the last open handle frees the process-wide restore staging (pinned
+ * window ring, per-device HBM window ring and scratch, up to ~4 GiB each). */
 void ts_restore_close(ts_restore* r);
+/* Frees that staging now (e.g. before training resumes while a handle stays
+ * open); returns the bytes freed. B200-side addition (no reference counterpart). */
+uint64_t ts_restore_release_staging(void);
 int ts_restore_n_ranks(ts_restore* r);
 ts_status ts_restore_rank_info(ts_restore* r, int index, ts_rank_info* out);
 /* Reads the footers of the rank's files and lists its objects in manifest order,
@@ -341,8 +346,10 @@ typedef struct ts_restore_stats {
 ts_status ts_restore_set_file_cache(ts_restore* r, int use);
 /* 1: fixed-region reads of files that are not page-locked go O_DIRECT from the
  * disk into the pinned windows (4 KiB-aligned bodies; ragged ends and
- * filesystems that refuse O_DIRECT, e.g. tmpfs, use pread). 0: pread.
- * -1 (default): O_DIRECT for files mostly absent from the page cache (cold). */
+ * filesystems that refuse O_DIRECT use pread; tmpfs never goes O_DIRECT, its
+ * "direct" reads are page-cache reads). 0: pread. -1 (default): O_DIRECT for
+ * files mostly absent from the page cache (cold; probed per file with
+ * preadv2(RWF_NOWAIT) on 64 sampled pages). */
 ts_status ts_restore_set_direct_io(ts_restore* r, int use);
 ts_status ts_restore_rank(ts_restore* r, int index, const ts_object_desc* dst, size_t n,
                           int device, void* stream, ts_restore_stats* stats);

@@ -17,7 +17,10 @@
 //   tmeta <oid> <file_id> <name> <dtype> <numel> <shard_off> <shard_len>
 // Payloads are materialized with the reference's own fill_pattern
 // (pattern.hpp:57-69) and make_metadata_value (model.cpp:206-231).
+#include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -141,14 +144,26 @@ recipe load_recipe(const std::string& path) {
 std::vector<rank_state>& ranks_of(recipe& r) { return r.is_layout ? r.layout.ranks : r.ranks; }
 
 void materialize(recipe& r) {
+  // (harness setup, not timed: the reference's fill_pattern per object, objects
+  // spread over the host threads this process may use)
   auto& ranks = ranks_of(r);
-  for (auto& rs : ranks) {
-    for (auto& o : rs.objects) {
-      if (!o.is_raw()) continue;
-      o.payload.resize(o.size_bytes);
-      fill_pattern(o.payload, pattern_key{rs.seed, o.pattern_space, r.pattern_it}, o.pattern_offset);
+  std::vector<std::pair<rank_state*, state_object*>> todo;
+  for (auto& rs : ranks)
+    for (auto& o : rs.objects)
+      if (o.is_raw()) todo.push_back({&rs, &o});
+  std::atomic<size_t> next{0};
+  auto work = [&] {
+    for (size_t k; (k = next++) < todo.size();) {
+      auto& [rs, o] = todo[k];
+      o->payload.resize(o->size_bytes);
+      fill_pattern(o->payload, pattern_key{rs->seed, o->pattern_space, r.pattern_it}, o->pattern_offset);
     }
-  }
+  };
+  const unsigned nt = std::max(1u, std::min<unsigned>(32, std::thread::hardware_concurrency()));
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < nt; ++t) th.emplace_back(work);
+  work();
+  for (auto& t : th) t.join();
   if (r.is_layout) {
     for (auto& rs : ranks)
       for (auto& o : rs.objects)
@@ -175,7 +190,8 @@ struct opts_t {
   uint64_t ser_chunk = default_serialized_chunk_bytes;
   int reps = 1;
   int warmup = 0;
-  bool restore = false;
+  bool restore = false;       // restore after every step
+  bool restore_last = false;  // restore once, after the last step
   std::string strategy = "lazy";
 };
 
@@ -349,7 +365,7 @@ int cmd_bench(recipe& r, const std::string& dir, const opts_t& o) {
       iss = std::max(iss, x.issue_ns);
     }
     double restore_s = -1;
-    if (o.restore) {
+    if (o.restore || (o.restore_last && s + 1 == o.warmup + o.reps)) {
       auto a = std::chrono::steady_clock::now();
       auto st = restore_checkpoint(std::filesystem::path(dir) / "MANIFEST.tlv");
       restore_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
@@ -428,6 +444,7 @@ int main(int argc, char** argv) {
     else if (a == "--reps") o.reps = std::stoi(next());
     else if (a == "--warmup") o.warmup = std::stoi(next());
     else if (a == "--restore") o.restore = true;
+    else if (a == "--restore-last") o.restore_last = true;
     else if (a == "--strategy") o.strategy = next();
     else die("unknown option " + a);
   }

@@ -24,4 +24,9 @@ uint64_t tso_mix64(uint64_t x);
  * returns tensor_region_end. order_out receives the planned order (indices). */
 uint64_t tso_plan_file(const uint64_t* ids, const uint64_t* sizes, size_t n, uint64_t alignment,
                        uint64_t* offsets_out, size_t* order_out);
+/* Bulk checkers (threaded; same arithmetic as above): FNV-1a of each object's
+ * pattern bytes, and FNV-1a of each [ptrs[i], ptrs[i] + lens[i]) range. */
+void tso_fnv_pattern_many(size_t n, const uint64_t* seed, const uint64_t* space, const uint64_t* iter,
+                          const uint64_t* offset, const uint64_t* size, int threads, uint64_t* out);
+void tso_fnv_ranges_many(size_t n, const uint8_t* const* ptrs, const uint64_t* lens, int threads, uint64_t* out);
 #endif

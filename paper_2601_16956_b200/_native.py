@@ -217,6 +217,7 @@ _sig("ts_ticket_object_checksum", i32, P, u64, C.POINTER(u64))
 _sig("ts_ticket_release", None, P)
 _sig("ts_restore_open", i32, C.c_char_p, C.POINTER(P))
 _sig("ts_restore_close", None, P)
+_sig("ts_restore_release_staging", C.c_uint64)
 _sig("ts_restore_n_ranks", i32, P)
 _sig("ts_restore_rank_info", i32, P, i32, C.POINTER(RankInfo))
 _sig("ts_restore_rank_objects", i32, P, i32, C.POINTER(RestoreObject), sz, C.POINTER(sz))

@@ -711,6 +711,11 @@ class Restorer:
         if h:
             _close(h)
 
+    def close(self):
+        """Closes the handle; the last open one frees the restore staging
+        (pinned ring + HBM window ring, up to ~4 GiB each)."""
+        self.__del__()
+
     @property
     def n_ranks(self) -> int:
         return N.lib.ts_restore_n_ranks(self.h)
@@ -761,6 +766,11 @@ class Restorer:
                 N.call(N.lib.ts_restore_structured, self.h, index, o.object_id, C.byref(out))
                 o.structured = Value(out.value).to_py()
         return rs
+
+
+def release_restore_staging() -> int:
+    """Frees the process-wide restore staging now; returns the bytes freed."""
+    return int(N.lib.ts_restore_release_staging())
 
 
 def restore_checkpoint(manifest_path: str, device: int = 0, stream=None) -> List[RankState]:

@@ -409,6 +409,7 @@ ts_status ts_restore_open(const char* manifest_path, ts_restore** out) {
 }
 
 void ts_restore_close(ts_restore* r) { delete r; }
+uint64_t ts_restore_release_staging(void) { return restore_release_staging(); }
 int ts_restore_n_ranks(ts_restore* r) { return static_cast<int>(r->r->m.ranks.size()); }
 
 ts_status ts_restore_rank_info(ts_restore* r, int index, ts_rank_info* out) {

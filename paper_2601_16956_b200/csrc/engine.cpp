@@ -541,8 +541,13 @@ std::shared_ptr<ticket_state> engine::issue(const std::shared_ptr<session>& sp, 
       }
       return fs.dma != nullptr;
     };
-    fs.w = std::make_unique<file_writer>(rdir + "/" + fname, fp.tensor_region_end, j->plan.hash,
-                                         cfg_.overwrite != 0, j->io, recycled, on_open);
+    try {
+      fs.w = std::make_unique<file_writer>(rdir + "/" + fname, fp.tensor_region_end, j->plan.hash,
+                                           cfg_.overwrite != 0, j->io, recycled, on_open);
+    } catch (...) {  // (header write / pre-size failed after the claim: give the entry back)
+      if (fs.claimed && !fs.released) file_registry::get().release(fs.key, -1, false);
+      throw;
+    }
     fs.append_end = fp.tensor_region_end;
     if (cfg_.flush_mmap == 2 && !fs.dma) fs.w->open_direct();
     else if (cfg_.flush_mmap && !fs.dma) fs.w->map_fixed_region();

@@ -5,6 +5,7 @@
 #include <sys/mman.h>
 #include <sys/stat.h>
 #include <sys/statvfs.h>
+#include <sys/vfs.h>
 #include <unistd.h>
 
 #include <dirent.h>
@@ -194,6 +195,10 @@ file_writer::~file_writer() {
 
 bool file_writer::open_direct() {
   if (!io_ || dfd_ >= 0 || map_) return dfd_ >= 0;
+  // tmpfs accepts O_DIRECT (Linux >= 6.6) but serves it from its page cache:
+  // nothing to bypass, keep the buffered path (and honest direct_io_bytes)
+  struct statfs fs;
+  if (::fstatfs(fd_, &fs) == 0 && static_cast<unsigned long>(fs.f_type) == 0x01021994ul) return false;
   dfd_ = ::open(path_.c_str(), O_WRONLY | O_DIRECT);
   return dfd_ >= 0;
 }
@@ -229,8 +234,16 @@ void file_writer::write_fixed(uint64_t off, const void* p, size_t n) {
   if (!io_ || n == 0) return;
   if (off < header_reserved || off + n > tre_) fail(TS_ERR_IO, "fixed write outside the tensor region");
   if (map_) {
-    std::memcpy(map_ + off, p, n);
-    return;
+    // Reserve the range before touching the mapping: a write fault on a full
+    // filesystem is a SIGBUS, a failed fallocate is an error we can report
+    // (the positional write below then returns ENOSPC as a format error, the
+    // reference's pwrite behaviour). Filesystems without fallocate keep the
+    // free-space check made at map time.
+    if (::fallocate(fd_, 0, static_cast<off_t>(off), static_cast<off_t>(n)) == 0 || errno == EOPNOTSUPP ||
+        errno == ENOSYS) {
+      std::memcpy(map_ + off, p, n);
+      return;
+    }
   }
   const auto* b = static_cast<const uint8_t*>(p);
   constexpr uint64_t blk = 4096;

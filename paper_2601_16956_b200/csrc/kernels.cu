@@ -357,11 +357,16 @@ void launch_pack(const seg* d_segs, uint32_t nsegs, uint64_t lo, uint64_t hi, ui
 void launch_pack_bulk(const bulk_job* d_jobs, uint32_t njobs, uint64_t lo, uint8_t* dst, int ctas,
                       cudaStream_t st) {
   if (njobs == 0) return;
-  static bool attr = false;
+  // The dynamic shared memory opt-in is per device: one process may drive
+  // engines (or helper streams) on several GPUs.
+  static std::atomic<uint64_t> attr_set{0};
   const int smem = kBulkStages * static_cast<int>(kBulkJob);
-  if (!attr) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_set.load() & bit)) {
     cudaFuncSetAttribute(pack_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
+    attr_set.fetch_or(bit);
   }
   const int grid = static_cast<int>(std::min<uint64_t>(njobs, static_cast<uint64_t>(ctas)));
   pack_bulk_kernel<<<grid, 32, smem, st>>>(d_jobs, njobs, lo, dst);

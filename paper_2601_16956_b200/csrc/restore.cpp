@@ -2,6 +2,8 @@
 //   files --pread--> pinned window ring --H2D--> HBM window ring --unpack--> shards
 // with per-object FNV verification on host threads overlapping the transfers.
 #include <fcntl.h>
+#include <sys/uio.h>
+#include <sys/vfs.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -34,22 +36,32 @@ struct fd_holder {
 };
 
 // True when fewer than half of 64 sampled pages of [0, len) are in the page
-// cache (mincore over a read-only mapping): a cold file on a disk, where
-// O_DIRECT reads beat pread (measured 3.8-4.0 vs 1.6-2.8 GB/s); warm files
-// (just written) stay on pread from the page cache.
+// cache: a cold file on a disk, where O_DIRECT reads beat pread (measured
+// 3.8-4.0 vs 1.6-2.8 GB/s); warm files (just written) stay on pread from the
+// page cache. Probed with preadv2(RWF_NOWAIT), which fails with EAGAIN for a
+// page that is not cached whatever the caller's permissions on the file
+// (mincore over a mapping reports page-cache state only to callers that could
+// write the file, Linux >= 5.2, so read-only checkpoints would be misjudged).
 bool mostly_uncached(int fd, uint64_t len) {
   if (len < (8ull << 20)) return false;
-  void* m = ::mmap(nullptr, len, PROT_READ, MAP_SHARED, fd, 0);
-  if (m == MAP_FAILED) return false;
   const uint64_t pg = 4096, pages = len / pg;
-  int resident = 0;
+  int resident = 0, answered = 0;
   for (int i = 0; i < 64; ++i) {
     unsigned char v = 0;
+    struct iovec io = {&v, 1};
     const uint64_t at = (pages * static_cast<uint64_t>(2 * i + 1) / 128) * pg;
-    if (::mincore(static_cast<uint8_t*>(m) + at, pg, &v) == 0 && (v & 1)) ++resident;
+    const ssize_t k = ::preadv2(fd, &io, 1, static_cast<off_t>(at), RWF_NOWAIT);
+    if (k == 1) ++resident, ++answered;
+    else if (k < 0 && errno == EAGAIN) ++answered;
   }
-  ::munmap(m, len);
-  return resident < 32;
+  return answered == 64 && resident < 32;  // (no RWF_NOWAIT support: stay on pread)
+}
+
+// tmpfs serves O_DIRECT from its page cache (Linux >= 6.6 accepts the flag):
+// there is nothing to bypass, so O_DIRECT is never used on it.
+bool on_tmpfs(int fd) {
+  struct statfs fs;
+  return ::fstatfs(fd, &fs) == 0 && static_cast<unsigned long>(fs.f_type) == 0x01021994ul;
 }
 
 // Reads [off, off+n) of a file into p: the 4 KiB-aligned body O_DIRECT when
@@ -73,8 +85,11 @@ void read_range(const fd_holder& f, uint8_t* p, uint64_t n, uint64_t off, const 
   pread_all(f.fd, p, n, off, path);
 }
 
-// Process-wide staging reused across restores (pinning is slow; allocate once).
+// Process-wide staging reused across restores while any restore handle is
+// open (pinning and multi-GB allocations are slow); freed when the last one
+// closes, so training after a restore gets its HBM and host memory back.
 std::mutex g_stage_mu;
+int g_stage_users = 0;
 uint8_t* g_pinned = nullptr;
 uint64_t g_pinned_bytes = 0;
 
@@ -108,7 +123,43 @@ uint8_t* pinned_stage(uint64_t bytes) {
   return g_pinned;
 }
 
+void release_staging_locked() {
+  if (g_pinned) cudaFreeHost(g_pinned);
+  g_pinned = nullptr;
+  g_pinned_bytes = 0;
+  for (auto* m : {&g_dev_stage, &g_dev_scratch, &g_dev_fnv}) {
+    for (auto& [dev, e] : *m) {
+      if (!e.first) continue;
+      cudaSetDevice(dev);
+      cudaFree(e.first);
+    }
+    m->clear();
+  }
+}
+
 }  // namespace
+
+uint64_t restore_release_staging() {
+  std::lock_guard<std::mutex> g(g_stage_mu);
+  uint64_t b = g_pinned_bytes;
+  for (auto* m : {&g_dev_stage, &g_dev_scratch, &g_dev_fnv})
+    for (auto& kv : *m) b += kv.second.second;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  release_staging_locked();
+  cudaSetDevice(cur);
+  return b;
+}
+
+restore_handle::~restore_handle() {
+  std::lock_guard<std::mutex> g(g_stage_mu);
+  if (--g_stage_users == 0) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    release_staging_locked();
+    cudaSetDevice(cur);
+  }
+}
 
 void restore_handle::load_rank(int index) {
   auto& rc = ranks.at(static_cast<size_t>(index));
@@ -156,6 +207,8 @@ restore_handle::restore_handle(const std::string& manifest_path) {
   const auto slash = manifest_path.find_last_of('/');
   base = slash == std::string::npos ? "." : manifest_path.substr(0, slash);
   ranks.resize(m.ranks.size());
+  std::lock_guard<std::mutex> g(g_stage_mu);
+  ++g_stage_users;
 }
 
 namespace {
@@ -259,13 +312,11 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
   // roofline vs 82-85 % at 256 MiB; small restores keep small staging)
   const int K = 4;
   const uint64_t W = std::min<uint64_t>(1ull << 30, std::max<uint64_t>(64ull << 20, align_up(img / K + 1, 2ull << 20)));
-  uint8_t* hring;
-  {
-    std::lock_guard<std::mutex> g(g_stage_mu);
-    hring = pinned_stage(W * K);
-  }
+  // One restore at a time uses the rings: take the lock first and size them
+  // under it, so a concurrent restore cannot reallocate them in between.
+  std::lock_guard<std::mutex> stage_guard(g_stage_mu);
+  uint8_t* hring = pinned_stage(W * K);
   rtrace("pinned stage", t_begin);
-  std::lock_guard<std::mutex> stage_guard(g_stage_mu);  // one restore at a time uses the ring
   uint8_t* dring = nullptr;
   dev::useg* d_usegs = nullptr;
   dring = device_stage(device, W * K);
@@ -340,8 +391,9 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
   for (size_t k = 0; k < rc.files.size(); ++k) {
     fds[k].fd = ::open(rc.files[k].path.c_str(), O_RDONLY);
     if (fds[k].fd < 0) fail(TS_ERR_MISSING_FILE, "cannot open " + rc.files[k].path);
-    if (direct_io > 0 || (direct_io < 0 && mostly_uncached(fds[k].fd, rc.files[k].region_end)))
-      fds[k].dfd = ::open(rc.files[k].path.c_str(), O_RDONLY | O_DIRECT);  // -1 (tmpfs): pread
+    if (!on_tmpfs(fds[k].fd) &&
+        (direct_io > 0 || (direct_io < 0 && mostly_uncached(fds[k].fd, rc.files[k].region_end))))
+      fds[k].dfd = ::open(rc.files[k].path.c_str(), O_RDONLY | O_DIRECT);  // -1 (refused): pread
   }
   // Page-locked files (registered by this process's engines): H2D straight
   // from the page cache, no pread. Pinned against claims/drops until the end.

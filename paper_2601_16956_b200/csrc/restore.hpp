@@ -36,10 +36,17 @@ struct restore_handle {
   int direct_io = -1;
 
   explicit restore_handle(const std::string& manifest_path);
+  ~restore_handle();
+  restore_handle(const restore_handle&) = delete;
+  restore_handle& operator=(const restore_handle&) = delete;
   void load_rank(int index);
   void restore_rank(int index, const ts_object_desc* dst, size_t n, int device, cudaStream_t st,
                     ts_restore_stats* stats);
 };
+
+// Frees the process-wide restore staging (pinned ring, per-device window ring,
+// scratch); returns the bytes freed. Also done when the last handle closes.
+uint64_t restore_release_staging();
 
 void verify_checkpoint(const std::string& manifest_path, std::vector<std::pair<int, int64_t>>& issues,
                        uint64_t& files_checked, uint64_t& objects_checked);

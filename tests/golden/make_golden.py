@@ -158,6 +158,9 @@ def main():
            ("cfg1b", S.config_recipe("cfg1b"), None, True),
            ("cfg2_rank0", S.config_recipe("cfg2", 0), [0], False),
            ("cfg3_rank0", S.config_recipe("cfg3", 0), [0], False)]
+    # cfg2 ranks 1-7 (ZeRO-1 optimizer shards only, 10.1 GB each; the params
+    # are written by dp 0, model.cpp:124)
+    big += [(f"cfg2_rank{r}", S.config_recipe("cfg2", r), [r], False) for r in range(1, 8)]
     for name, rec, ranks, with_manifest in big:
         if args.only and name != args.only:
             continue

@@ -131,3 +131,83 @@ def test_oracle_detects_tamper_truncation_and_bad_manifest(oracle, tmp_path):
     with pytest.raises(oracle.FormatError) as ei:
         oracle.read_manifest(str(d / "MANIFEST.tlv"))
     assert ei.value.kind == "bad_manifest"
+
+
+@pytest.mark.parametrize("name", golden_recipes())
+def test_rank_digest_verifies_reference_tree(oracle, name):
+    """The file-free digest (oracle/tso.py rank_digest, used for cfg4) describes
+    every reference-written golden tree exactly, and the full-size structural
+    verifier (tests/gpu_helpers.py) accepts those trees."""
+    from gpu_helpers import verify_files_against_digest
+
+    rec = oracle.load_recipe(os.path.join(GOLDEN, "recipes", name + ".recipe"))
+    files, infos = {}, []
+    for r in rec.ranks:
+        f, info = oracle.rank_digest(r, rec.pit, threads=2)
+        files.update(f)
+        infos.append(info)
+    m = oracle.tlv_encode(oracle.manifest_value(rec.ckpt_id, rec.iteration, rec.manifest_echo(), infos))
+    import hashlib
+
+    files["MANIFEST.tlv"] = {"size": len(m), "sha256": hashlib.sha256(m).hexdigest()}
+    root = os.path.join(GOLDEN, "trees", name)
+    tree = read_tree(root)
+    assert sorted(tree) == sorted(files)
+    assert verify_files_against_digest(oracle, root, files, threads=2) == sum(
+        len(v) for k, v in tree.items() if k != "MANIFEST.tlv")
+
+
+def test_rank_digest_verifier_catches_one_flipped_byte(oracle, tmp_path):
+    from gpu_helpers import verify_files_against_digest
+
+    rec = oracle.load_recipe(os.path.join(GOLDEN, "recipes", "hand_mixed.recipe"))
+    root = str(tmp_path / "t")
+    shutil.copytree(os.path.join(GOLDEN, "trees", "hand_mixed"), root)
+    files, _ = oracle.rank_digest(rec.ranks[0], rec.pit, threads=2)
+    verify_files_against_digest(oracle, root, files, threads=2)
+    for rel, d in files.items():  # one byte in an object, in a gap, in the header
+        raws = [e for e in d["footer"] if e[1] == 0]
+        gap = next((e[2] + e[3] for e in raws if (e[2] + e[3]) % 4096 and e[2] + e[3] < d["tensor_region_end"]),
+                   None)
+        for pos in [p for p in (raws[0][2] + raws[0][3] // 2 if raws else None, gap, 100) if p is not None]:
+            p = os.path.join(root, rel)
+            with open(p, "r+b") as f:
+                f.seek(pos)
+                b = f.read(1)
+                f.seek(pos)
+                f.write(bytes([b[0] ^ 1]))
+            with pytest.raises(AssertionError):
+                verify_files_against_digest(oracle, root, files, threads=2)
+            with open(p, "r+b") as f:
+                f.seek(pos)
+                f.write(b)
+
+
+def test_cfg1_rank_digest_matches_reference_digest(oracle):
+    """rank_digest reproduces the reference-written full-size cfg1 digest (the
+    same restatement made the cfg4 digest; make_oracle_digests.py re-pins it on
+    every reference digest)."""
+    with open(os.path.join(GOLDEN, "digests", "cfg1.json")) as f:
+        ref = json.load(f)
+    rec = oracle.load_recipe(os.path.join(GOLDEN, "recipes", "cfg1.recipe"))
+    files, _ = oracle.rank_digest(rec.ranks[0], rec.pit)
+    for rel, d in files.items():
+        assert d["size"] == ref["files"][rel]["size"]
+        assert d["footer"] == ref["files"][rel]["footer"]
+
+
+def test_cfg4_digest_is_the_oracles(oracle):
+    """The committed cfg4 digest's plan side (sizes, footer offsets, headers)
+    equals what the oracle derives from the cfg4 recipe (checksums are covered by
+    make_oracle_digests.py: 120 GB of hashing is too slow for the CPU suite)."""
+    with open(os.path.join(GOLDEN, "digests", "cfg4_rank0.json")) as f:
+        dig = json.load(f)
+    rec = oracle.load_recipe(os.path.join(GOLDEN, "recipes", "cfg4_rank0.recipe"))
+    r = rec.ranks[0]
+    plan = oracle.plan_layout(r.objects)
+    assert len([o for o in r.objects if o.kind == 0]) == 2892 and len(r.objects) == 3616
+    for fid, fp in plan.items():
+        d = dig["files"][f"rank_0000/file_{fid}.bin"]
+        assert d["tensor_region_end"] == fp.tensor_region_end
+        assert [(e[0], e[2], e[3]) for e in d["footer"] if e[1] == 0] == sorted(fp.fixed, key=lambda x: x[1])
+        assert d["header"][24:40] == oracle.plan_hash(plan).to_bytes(8, "little").hex()
