@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import shutil
 import statistics
@@ -279,45 +280,66 @@ def reference_arm(args):
     print(json.dumps(line))
 
 
-def gemm_load(ms: float, dev, graph: bool = False):
-    """Synthetic forward/backward: back-to-back bf16 GEMMs for ~ms milliseconds,
-    launched eagerly from Python or replayed as one CUDA graph."""
+def gemm_load(ms: float, dev, graph: bool = False, hbm_frac: float = 0.0):
+    """Synthetic forward/backward for ~ms milliseconds: back-to-back bf16 GEMMs
+    (compute-bound) interleaved, in 8 layer-like blocks, with an HBM-bound
+    elementwise phase (bf16 a + b over 1 GiB operands: ~3 B of HBM traffic per
+    element, the norm/activation/optimizer-style kernels of a real step) taking
+    `hbm_frac` of the time; launched eagerly from Python or replayed as one
+    CUDA graph."""
     import torch
 
     n = 8192
     a = torch.randn(n, n, device=dev, dtype=torch.bfloat16)
     b = torch.randn(n, n, device=dev, dtype=torch.bfloat16)
+    c = torch.empty(n, n, device=dev, dtype=torch.bfloat16)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for _ in range(3):
-        a @ b
-    e0.record()
-    for _ in range(10):
-        a @ b
-    e1.record()
-    e1.synchronize()
-    per = e0.elapsed_time(e1) / 10
-    reps = max(1, int(ms / per))
+
+    def per_call(fn):
+        for _ in range(3):
+            fn()
+        e0.record()
+        for _ in range(10):
+            fn()
+        e1.record()
+        e1.synchronize()
+        return e0.elapsed_time(e1) / 10
+
+    gemm = lambda: torch.matmul(a, b, out=c)  # noqa: E731
+    per_g = per_call(gemm)
+    ew, per_e = None, 0.0
+    if hbm_frac > 0:
+        m = 1 << 29  # 512 Mi bf16 = 1 GiB per operand (>> L2)
+        x = torch.randn(m, device=dev, dtype=torch.bfloat16)
+        y = torch.randn(m, device=dev, dtype=torch.bfloat16)
+        z = torch.empty(m, device=dev, dtype=torch.bfloat16)
+        ew = lambda: torch.add(x, y, out=z)  # noqa: E731
+        per_e = per_call(ew)
+    blocks = 8
+    reps_g = max(1, int(ms * (1 - hbm_frac) / per_g / blocks))
+    reps_e = max(1, int(ms * hbm_frac / per_e / blocks)) if ew else 0
+
+    def body():
+        for _ in range(blocks):
+            for _ in range(reps_g):
+                gemm()
+            for _ in range(reps_e):
+                ew()
+
+    total = blocks * (reps_g * per_g + reps_e * per_e)
     if graph:
-        c = torch.empty(n, n, device=dev, dtype=torch.bfloat16)
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
-            for _ in range(3):
-                torch.matmul(a, b, out=c)
+            gemm()
+            if ew:
+                ew()
         torch.cuda.current_stream().wait_stream(side)
         with torch.cuda.graph(g):
-            for _ in range(reps):
-                torch.matmul(a, b, out=c)
-        return g.replay, reps * per
-
-    def run():
-        c = None
-        for _ in range(reps):
-            c = a @ b
-        return c
-
-    return run, reps * per
+            body()
+        return g.replay, total
+    return body, total
 
 
 def ours(args):
@@ -385,7 +407,7 @@ def ours(args):
                            checksum_priority=args.ck_priority, pack_priority=args.pack_priority,
                            checksum_host_frac=args.ck_host_frac, ring_chunk_bytes=int(args.ring_chunk_gb * (1 << 30)),
                            worker_nice=args.worker_nice, helper_devices=helpers, helper_share=share,
-                           flush_mmap=2 if args.flush_direct else int(not args.flush_pwrite))
+                           flush_mmap=3 if args.flush_uring else 2 if args.flush_direct else int(not args.flush_pwrite))
     eng = api.CheckpointEngine(cfg, spec.rank_id, local_dev)
     numa_node = eng.numa_node
     full = getattr(rec, "full_layout", None)
@@ -598,7 +620,7 @@ def ours(args):
     # --- training-blocked time with a synthetic fwd/bwd load ------------------
     blocked = None
     if args.train_steps > 0:
-        blocked = training_phase(args, api, state, spec, cfg, local_dev, dev, it)
+        blocked = training_phase(args, api, state, spec, cfg, local_dev, dev, it, statistics.mean(snap_ms))
 
     # the TMA bulk kernel runs only for a full device shadow (engine.cpp run_job);
     # a multi-slot HBM ring (cfg4) packs every chunk with the warp kernel
@@ -653,13 +675,19 @@ def ours(args):
         dist.destroy_process_group()
 
 
-def training_phase(args, api, state, spec, cfg, local, dev, it0):
+def training_phase(args, api, state, spec, cfg, local, dev, it0, snap_ms):
     """fwd+bwd (bf16 GEMMs) -> pre_update_barrier -> update -> issue, with and
     without checkpointing; reports host-blocked ms per checkpoint (issue_block +
     barrier_block, simulator.cpp:211-212) and the step-time slowdown."""
     import torch
 
-    run, fb_ms = gemm_load(args.fwd_bwd_ms, dev, graph=args.fwd_bwd == "graph")
+    run, fb_ms = gemm_load(args.fwd_bwd_ms, dev, graph=args.fwd_bwd == "graph", hbm_frac=args.hbm_frac)
+    # Checkpoint cadence: --ckpt-interval, or (0, default) the most frequent one
+    # the D2H link sustains: a snapshot (measured above) must fit, with 10 %
+    # margin, into the steps between two checkpoints. A 120.7 GB shard over one
+    # PCIe Gen5 x16 link takes ~2.2 s, longer than a 1.8 s step: every 2 steps.
+    interval = args.ckpt_interval or max(1, math.ceil(1.1 * snap_ms / fb_ms))
+    n_steps = -(-args.train_steps // interval) * interval  # whole checkpoint cycles per timed block
     # Long-lived objects (thousands of state descriptors) out of the cyclic GC's
     # reach, as training loops do: a full collection over them landed inside
     # random issue calls (up to ~270 ms for cfg4's 3,616 objects).
@@ -680,6 +708,11 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
         shutil.rmtree(tdir, ignore_errors=True)
         os.makedirs(tdir)
         cfg = api.EngineConfig(**{**cfg.__dict__, "write_files": True})
+    # comparison strategies (engine.cpp:575-613): lazy (default), DataStates-Old
+    # (lazy, structured objects serialized inline at issue), two_phase, sync
+    strat = {"lazy": ("lazy", True), "lazy_old": ("lazy", False), "two_phase": ("two_phase", True),
+             "sync": ("sync", True)}[args.strategy]
+    cfg = api.EngineConfig(**{**cfg.__dict__, "strategy": strat[0], "lazy_serialize_overlap": strat[1]})
     eng = api.CheckpointEngine(cfg, spec.rank_id, local)
     spare = os.path.join(tdir, ".spare")
     if files:
@@ -687,7 +720,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
     ckpts = []  # (dir, session, ticket) on disk, oldest first
     comp = torch.cuda.current_stream()
     res = {"off": ([], []), "lazy": ([], [])}
-    host_ck = []
+    host_ck, ck_tickets = [], []
     issue_cpp, issue_py = [], []  # issue time inside the engine vs the whole Python call
     clk = {"off": [], "lazy": []}
     fb_gpu = {"off": [], "lazy": []}  # CUDA-event time of fwd+bwd on the compute stream
@@ -726,7 +759,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
         times, blocked = res[mode]
         sampler = Clocks(local)
         sampler.__enter__()
-        for k in range(args.train_steps + 1):
+        for k in range(n_steps + 1):
             comp.synchronize()  # like a per-step loss.item(): the compute stream only, never the device
             t0 = time.perf_counter()
             ev0.record(comp)
@@ -742,7 +775,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
             api.mutate_update_step(state, it, stream=comp)  # optimizer update
             p_upd = time.perf_counter()
             ib = 0
-            if mode == "lazy" and k % args.ckpt_interval == 0:
+            if mode == "lazy" and k % interval == 0:
                 if files:
                     d, sess = rotate_and_issue(it)
                 else:
@@ -754,7 +787,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
                     ckpts.append((d, sess, pending))
                 if k > 0:
                     st_k = pending.stats()
-                    host_ck.append(st_k["host_checksum_bytes"] / max(1, spec.raw_bytes))
+                    ck_tickets.append(pending)  # (checksum placement is known once prepared: read at the end)
                     issue_cpp.append(st_k["issue_block_ns"] / 1e6)
                     issue_py.append(1e3 * ib)
             p_iss = time.perf_counter()
@@ -763,7 +796,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
                 p_end = time.perf_counter()
                 times.append(p_end - t0)
                 phases[mode].append((p_fb - t0, p_bar - p_fb, p_upd - p_bar, p_iss - p_upd, p_end - p_iss))
-                if mode == "lazy" and k % args.ckpt_interval == 0:
+                if mode == "lazy" and k % interval == 0:
                     blocked.append(1e3 * (b / 1e9 + ib))
                 elif b and blocked:
                     blocked[-1] += 1e3 * b / 1e9  # barrier wait attributed to its checkpoint
@@ -771,6 +804,10 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
         clk[mode].append(sampler.summary())
         if pending:
             pending.wait_persisted()
+        for tk in ck_tickets:
+            tk.wait_persisted()
+            host_ck.append(tk.stats()["host_checksum_bytes"] / max(1, spec.raw_bytes))
+        ck_tickets.clear()
     res = {m: (statistics.mean(t), statistics.mean(b) if b else 0.0) for m, (t, b) in res.items()}
     eng.shutdown()
     dma = [t.stats()["file_dma_bytes"] for _, _, t in ckpts]
@@ -779,8 +816,11 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0):
         shutil.rmtree(tdir, ignore_errors=True)
         api.file_cache_release_all()
     off, lazy = res["off"][0], res["lazy"][0]
-    return {"fwd_bwd_ms": round(fb_ms, 1), "fwd_bwd_launch": args.fwd_bwd, "steps": 2 * args.train_steps,
-            "ckpt_interval": args.ckpt_interval,
+    return {"fwd_bwd_ms": round(fb_ms, 1), "fwd_bwd_launch": args.fwd_bwd, "steps": 2 * n_steps,
+            "ckpt_interval": interval,
+            "ckpt_interval_rule": ("--ckpt-interval" if args.ckpt_interval else
+                                   f"auto: ceil(1.1 x snapshot {snap_ms:.0f} ms / fwd+bwd {fb_ms:.0f} ms)"),
+            "hbm_bound_frac": args.hbm_frac, "strategy": args.strategy,
             "step_ms_no_ckpt": round(1e3 * off, 2), "step_ms_lazy_ckpt": round(1e3 * lazy, 2),
             "slowdown_pct": round(100 * (lazy - off) / off, 2),
             "blocked_ms_per_ckpt": round(res["lazy"][1], 3),
@@ -809,11 +849,17 @@ def main():
                          "cfg1, cfg1b, cfg2, cfg3")
     ap.add_argument("--mode", default="ring", choices=["ring", "direct", "zerocopy"])
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--train-steps", type=int, default=3)
+    ap.add_argument("--train-steps", type=int, default=4,
+                    help="timed steps per off/lazy block (rounded up to whole checkpoint cycles)")
     ap.add_argument("--fwd-bwd-ms", type=float, default=1800.0)
     ap.add_argument("--fwd-bwd", default="graph", choices=["graph", "eager"],
                     help="synthetic fwd/bwd launched as one CUDA graph (default) or eagerly from Python")
-    ap.add_argument("--ckpt-interval", type=int, default=1, help="checkpoint every k training steps")
+    ap.add_argument("--ckpt-interval", type=int, default=0,
+                    help="checkpoint every k training steps (0 = auto: the most frequent cadence the D2H sustains)")
+    ap.add_argument("--strategy", default="lazy", choices=["lazy", "lazy_old", "two_phase", "sync"],
+                    help="training phase: checkpoint strategy (the reference's comparison arms)")
+    ap.add_argument("--hbm-frac", type=float, default=0.35,
+                    help="share of the synthetic fwd/bwd spent in an HBM-bound elementwise phase")
     ap.add_argument("--host-checksum", action="store_true", help="FNV on host threads instead of the GPU kernels")
     ap.add_argument("--pack-kernel", default="bulk", choices=["warp", "bulk"],
                     help="bulk: TMA cp.async.bulk for large 16-B aligned fragments + warp kernel for the rest")
@@ -827,6 +873,8 @@ def main():
     ap.add_argument("--flush-pwrite", action="store_true", help="pool flushes with pwrite(2) instead of mmap copies")
     ap.add_argument("--flush-direct", action="store_true",
                     help="pool flushes with O_DIRECT pwrite from the pinned windows (disk filesystems)")
+    ap.add_argument("--flush-uring", action="store_true",
+                    help="as --flush-direct, each window body submitted through io_uring (4 MiB writes in flight)")
     ap.add_argument("--window-mb", type=int, default=64, help="D2H window (raw_chunk_bytes) in MiB")
     ap.add_argument("--no-train-files", dest="train_files", action="store_false",
                     help="training phase: snapshot only (no files)")

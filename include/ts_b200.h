@@ -174,7 +174,10 @@ typedef struct ts_engine_config {
                                        of the file (parallel per file); 0: pwrite(2); 2: O_DIRECT
                                        pwrite of each window's 4 KiB-aligned body straight from the
                                        pinned pool (page cache bypassed; disks), buffered where
-                                       the filesystem refuses O_DIRECT (tmpfs) */
+                                       the filesystem refuses O_DIRECT (tmpfs); 3: as 2, each body
+                                       submitted through the flush thread's io_uring as 4 MiB
+                                       writes in flight together (pwrite where io_uring is
+                                       unavailable) */
   int32_t pack_kernel;              /* RING pack: 1 (default) = TMA bulk copies (cp.async.bulk
                                        through shared memory) for 16-B aligned fragments >=
                                        bulk_min_bytes, warp kernel for the rest; 0 = warp gather
@@ -302,6 +305,12 @@ ts_status ts_ticket_stats_get(ts_ticket* t, ts_ticket_stats* out);
 /* Per-object checksum accumulated at staging (transfer.cpp:163-166) */
 ts_status ts_ticket_object_checksum(ts_ticket* t, uint64_t object_id, uint64_t* out);
 void ts_ticket_release(ts_ticket* t);
+/* Hands `n` structured values the caller passed to ts_issue over to the ticket:
+ * they are freed once the ticket is released AND its job has finished with
+ * them, so a non-blocking caller need not keep them alive until the snapshot
+ * (the reference's rank_state owns its values for the job's duration,
+ * engine.cpp:563-565). B200-side addition. */
+ts_status ts_ticket_adopt_values(ts_ticket* t, ts_value* const* values, size_t n);
 
 /* ------------------------------------------------------------------------ */
 /* Restore (format.cpp:201-494)                                              */
@@ -350,7 +359,11 @@ ts_status ts_restore_set_file_cache(ts_restore* r, int use);
  * "direct" reads are page-cache reads). 0: pread. -1 (default): O_DIRECT for
  * files mostly absent from the page cache (cold; probed per file with
  * preadv2(RWF_NOWAIT) on 64 sampled pages). */
-ts_status ts_restore_set_direct_io(ts_restore* r, int use);
+ts_status ts_restore_set_direct_io(ts_restore* r, int use); /* 2: O_DIRECT via io_uring */
+/* io_uring diagnostics (B200-side): 1 when this process can create a ring;
+ * requests submitted through io_uring so far (flush_mmap = 3, direct_io = 2). */
+int ts_io_uring_available(void);
+uint64_t ts_io_uring_ops(void);
 ts_status ts_restore_rank(ts_restore* r, int index, const ts_object_desc* dst, size_t n,
                           int device, void* stream, ts_restore_stats* stats);
 ts_status ts_restore_structured(ts_restore* r, int index, uint64_t object_id, ts_value** out);

@@ -215,6 +215,9 @@ _sig("ts_ticket_wait_persisted", i32, P, C.POINTER(i64))
 _sig("ts_ticket_stats_get", i32, P, C.POINTER(TicketStats))
 _sig("ts_ticket_object_checksum", i32, P, u64, C.POINTER(u64))
 _sig("ts_ticket_release", None, P)
+_sig("ts_ticket_adopt_values", i32, P, C.POINTER(P), C.c_size_t)
+_sig("ts_io_uring_available", i32)
+_sig("ts_io_uring_ops", u64)
 _sig("ts_restore_open", i32, C.c_char_p, C.POINTER(P))
 _sig("ts_restore_close", None, P)
 _sig("ts_restore_release_staging", C.c_uint64)

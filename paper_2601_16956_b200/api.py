@@ -22,6 +22,11 @@ from typing import Any, Dict, List, Optional
 import torch
 
 from . import _native as N
+
+try:  # CPython fast path of _desc_array (built next to libts_b200.so by build.py)
+    from . import _pyfast
+except ImportError:  # pragma: no cover - the pure-Python path is complete, only slower
+    _pyfast = None
 from .synthetic import Recipe, RankSpec
 
 TIER_DEVICE, TIER_HOST, TIER_PERSISTENT = 0, 1, 2
@@ -288,6 +293,15 @@ class RankState:
 
 def _desc_array(rank: RankState, keep: list, need_payload: bool = True):
     arr = (N.ObjectDesc * max(1, len(rank.objects)))()
+    if _pyfast is not None:
+        # one C walk over the objects (csrc/pyfast); anything it does not take
+        # (unusual values, errors) goes the pure-Python way below
+        try:
+            _pyfast.fill_descs(rank.objects, C.addressof(arr), need_payload, Value, keep)
+            return arr
+        except Exception:
+            C.memset(arr, 0, C.sizeof(arr))
+            keep.clear()
     for i, o in enumerate(rank.objects):
         d = arr[i]
         d.object_id, d.kind, d.tier, d.precision, d.file_id = (o.object_id, o.kind, o.residency,
@@ -329,7 +343,7 @@ class EngineConfig:
     pack_priority: int = 1  # capture stream: 1 high (default), 0 normal, -1 low
     write_files: bool = True
     checksum_on_gpu: bool = True
-    flush_mmap: int = 1  # 1: copy into a shared mapping; 0: pwrite; 2: O_DIRECT body + pwrite head/tail
+    flush_mmap: int = 1  # 1: copy into a shared mapping; 0: pwrite; 2: O_DIRECT body + pwrite head/tail; 3: 2 via io_uring
     pack_kernel: str = "bulk"  # "bulk" (TMA cp.async.bulk for large aligned fragments + warp kernel) | "warp"
     bulk_min_bytes: int = 1 << 20
     file_dma: bool = True  # D2H straight into page-locked file pages when registered (rotation)
@@ -694,17 +708,19 @@ class Restorer:
     """restore_checkpoint split per rank: open the manifest, list a rank's
     objects, restore it into caller-provided (or freshly allocated) shards."""
 
-    def __init__(self, manifest_path: str, use_file_cache: bool = True, direct_io: Optional[bool] = None):
+    def __init__(self, manifest_path: str, use_file_cache: bool = True, direct_io=None):
         """`use_file_cache`: read files this process page-locked (file_dma
         rotation) straight from their page cache; False: always pread.
-        `direct_io`: other files' fixed regions are read O_DIRECT (disks);
-        None (default): only files mostly absent from the page cache."""
+        `direct_io`: True: other files' fixed regions are read O_DIRECT (disks);
+        "uring": O_DIRECT through each reader thread's io_uring; False: pread;
+        None (default): O_DIRECT only for files mostly absent from the page cache."""
         h = C.c_void_p()
         N.call(N.lib.ts_restore_open, manifest_path.encode(), C.byref(h))
         self.h = h.value
         self.last_stats: Dict[str, Any] = {}
         N.call(N.lib.ts_restore_set_file_cache, self.h, int(use_file_cache))
-        N.call(N.lib.ts_restore_set_direct_io, self.h, -1 if direct_io is None else int(direct_io))
+        dio = -1 if direct_io is None else 2 if direct_io == "uring" else int(bool(direct_io))
+        N.call(N.lib.ts_restore_set_direct_io, self.h, dio)
 
     def __del__(self, _close=N.lib.ts_restore_close):
         h, self.h = getattr(self, "h", None), None

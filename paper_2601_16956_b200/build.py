@@ -24,6 +24,34 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3,-pthread,-W
           "-I" + os.path.join(os.path.dirname(HERE), "include")]
 
 
+PYFAST_SRC = os.path.join(CSRC, "pyfast", "pyfast.cpp")
+
+
+def pyfast_path() -> str:
+    import sysconfig
+
+    return os.path.join(HERE, "_pyfast" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_pyfast() -> str:
+    """The Python mirror's CPython fast path (csrc/pyfast): a host-only
+    extension linked against libts_b200.so (rpath $ORIGIN/_lib)."""
+    import sysconfig
+
+    out = pyfast_path()
+    deps = [PYFAST_SRC, LIB, os.path.join(os.path.dirname(HERE), "include", "ts_b200.h")]
+    if os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(d) for d in deps):
+        return out
+    cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-shared", "-fPIC", "-Wall",
+           "-I" + sysconfig.get_paths()["include"], "-I" + os.path.join(os.path.dirname(HERE), "include"),
+           PYFAST_SRC, "-o", out + ".tmp", "-L" + OUT_DIR, "-lts_b200", "-Wl,-rpath,$ORIGIN/_lib"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"pyfast build failed:\n{r.stderr}")
+    os.replace(out + ".tmp", out)
+    return out
+
+
 def sources():
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
 
@@ -58,6 +86,7 @@ def build(verbose: bool = False) -> str:
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
         os.replace(LIB + ".tmp", LIB)
+    build_pyfast()
     return LIB
 
 

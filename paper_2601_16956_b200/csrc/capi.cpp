@@ -6,6 +6,7 @@
 
 #include "engine.hpp"
 #include "restore.hpp"
+#include "uring.hpp"
 
 using namespace tsb;
 
@@ -385,6 +386,15 @@ ts_status ts_ticket_object_checksum(ts_ticket* t, uint64_t object_id, uint64_t* 
 
 void ts_ticket_release(ts_ticket* t) { delete t; }
 
+ts_status ts_ticket_adopt_values(ts_ticket* t, ts_value* const* values, size_t n) {
+  return guard([&] {
+    if (!t || (n && !values)) fail(TS_ERR_INVALID_ARG, "adopt_values: null argument");
+    std::lock_guard<std::mutex> g(t->t->mu);
+    for (size_t i = 0; i < n; ++i)
+      if (values[i]) t->t->owned_values.emplace_back(V(values[i]));
+  });
+}
+
 // --- restore / verify --------------------------------------------------------
 
 ts_status ts_restore_set_file_cache(ts_restore* r, int use) {
@@ -392,7 +402,7 @@ ts_status ts_restore_set_file_cache(ts_restore* r, int use) {
 }
 
 ts_status ts_restore_set_direct_io(ts_restore* r, int use) {
-  return guard([&] { r->r->direct_io = use < 0 ? -1 : use != 0; });
+  return guard([&] { r->r->direct_io = use < 0 ? -1 : use >= 2 ? 2 : use != 0; });
 }
 
 ts_status ts_restore_open(const char* manifest_path, ts_restore** out) {
@@ -410,6 +420,8 @@ ts_status ts_restore_open(const char* manifest_path, ts_restore** out) {
 
 void ts_restore_close(ts_restore* r) { delete r; }
 uint64_t ts_restore_release_staging(void) { return restore_release_staging(); }
+int ts_io_uring_available(void) { return uring_available() ? 1 : 0; }
+uint64_t ts_io_uring_ops(void) { return uring_ops(); }
 int ts_restore_n_ranks(ts_restore* r) { return static_cast<int>(r->r->m.ranks.size()); }
 
 ts_status ts_restore_rank_info(ts_restore* r, int index, ts_rank_info* out) {

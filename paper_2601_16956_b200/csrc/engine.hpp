@@ -109,6 +109,9 @@ struct ticket_state {
               ev_d2h_last = nullptr, ev_pack0 = nullptr;
   int device = 0;
   std::unordered_map<uint64_t, uint64_t> checksums;
+  // structured values handed over by the caller (ts_ticket_adopt_values): the
+  // job holds the ticket, so they outlive every serializer that reads them
+  std::vector<std::unique_ptr<value>> owned_values;
 
   ~ticket_state();
   void fail(ts_status s, const std::string& m, int64_t oid = -1);
@@ -149,6 +152,7 @@ class engine {
 
  private:
   friend struct job;
+  void prepare(const std::shared_ptr<job>& j, const ts_rank_info& rank, const ts_object_desc* objs, size_t n);
   void copier_loop();
   void completer_loop();
   void run_job(const std::shared_ptr<job>& j);
@@ -208,6 +212,7 @@ class engine {
   std::deque<pending_window> inflight_;
   bool stopping_ = false, copier_done_ = false;
   std::shared_ptr<job> last_job_;
+  std::vector<std::shared_ptr<job>> retired_;  // dropped by the copier (under mu_)
   std::string spare_dir_;  // recycled files of retired checkpoints (retire_checkpoint)
   // checksum placement (auto): host hashing capacity, measured per job
   double host_rate_ = 0, chain_rate_ = 0.45e9, slack_s_ = 0;

@@ -1,5 +1,6 @@
 // Layout planner, file format and manifest (see format.hpp for the contract).
 #include "format.hpp"
+#include "uring.hpp"
 
 #include <fcntl.h>
 #include <sys/mman.h>
@@ -253,8 +254,9 @@ void file_writer::write_fixed(uint64_t off, const void* p, size_t n) {
     const uint64_t a = (off + blk - 1) & ~(blk - 1), e = (off + n) & ~(blk - 1);
     if (e > a) {
       if (a > off) pwrite_all(fd_, b, a - off, off, path_);
-      const ssize_t k = ::pwrite(dfd_, b + (a - off), e - a, static_cast<off_t>(a));
-      if (k == static_cast<ssize_t>(e - a)) {
+      const int64_t k = uring_ ? uring_pwrite(dfd_, b + (a - off), e - a, a, 4ull << 20)
+                               : static_cast<int64_t>(::pwrite(dfd_, b + (a - off), e - a, static_cast<off_t>(a)));
+      if (k == static_cast<int64_t>(e - a)) {
         direct_bytes_ += e - a;
         if (off + n > e) pwrite_all(fd_, b + (e - off), off + n - e, e, path_);
         return;

@@ -80,6 +80,9 @@ class file_writer {
   // buffered writes stay) where the filesystem refuses O_DIRECT (tmpfs).
   bool open_direct();
   bool direct() const { return dfd_ >= 0; }
+  // O_DIRECT bodies go through this thread's io_uring (flush_mmap = 3): each
+  // window body as a batch of 4 MiB writes in flight together.
+  void use_uring(bool on) { uring_ = on; }
   uint64_t direct_bytes() const { return direct_bytes_.load(); }
   // Pre-faults [off, off+n) of the mapping (MADV_POPULATE_WRITE): page
   // allocation for the file overlaps the device-side capture and D2H.
@@ -96,6 +99,7 @@ class file_writer {
   std::string path_;
   int fd_ = -1;
   int dfd_ = -1;
+  bool uring_ = false;
   std::atomic<uint64_t> direct_bytes_{0};  // (flush threads of one file write concurrently)
   uint64_t tre_;
   bool io_;

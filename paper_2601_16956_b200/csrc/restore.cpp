@@ -16,6 +16,7 @@
 
 #include "engine.hpp"
 #include "restore.hpp"
+#include "uring.hpp"
 
 namespace tsb {
 
@@ -29,6 +30,7 @@ void rtrace(const char* what, int64_t t0) {
 struct fd_holder {
   int fd = -1;
   int dfd = -1;  // O_DIRECT descriptor (restore_handle::direct_io), else -1
+  bool uring = false;  // direct reads through the thread's io_uring (direct_io = 2)
   ~fd_holder() {
     if (dfd >= 0) ::close(dfd);
     if (fd >= 0) ::close(fd);
@@ -73,8 +75,9 @@ void read_range(const fd_holder& f, uint8_t* p, uint64_t n, uint64_t off, const 
   if (f.dfd >= 0 && ((reinterpret_cast<uintptr_t>(p) - off) & (blk - 1)) == 0) {
     const uint64_t a = (off + blk - 1) & ~(blk - 1), e = (off + n) & ~(blk - 1);
     if (e > a) {
-      const ssize_t k = ::pread(f.dfd, p + (a - off), e - a, static_cast<off_t>(a));
-      if (k == static_cast<ssize_t>(e - a)) {
+      const int64_t k = f.uring ? uring_pread(f.dfd, p + (a - off), e - a, a, 4ull << 20)
+                                : static_cast<int64_t>(::pread(f.dfd, p + (a - off), e - a, static_cast<off_t>(a)));
+      if (k == static_cast<int64_t>(e - a)) {
         *direct += e - a;
         if (a > off) pread_all(f.fd, p, a - off, off, path);
         if (off + n > e) pread_all(f.fd, p + (e - off), off + n - e, e, path);
@@ -394,6 +397,7 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
     if (!on_tmpfs(fds[k].fd) &&
         (direct_io > 0 || (direct_io < 0 && mostly_uncached(fds[k].fd, rc.files[k].region_end))))
       fds[k].dfd = ::open(rc.files[k].path.c_str(), O_RDONLY | O_DIRECT);  // -1 (refused): pread
+    fds[k].uring = fds[k].dfd >= 0 && direct_io == 2;
   }
   // Page-locked files (registered by this process's engines): H2D straight
   // from the page cache, no pread. Pinned against claims/drops until the end.

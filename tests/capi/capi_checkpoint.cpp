@@ -136,6 +136,11 @@ int main(int argc, char** argv) {
                    0, o.file, o.size, o.data, o.value});
     ts_ticket* t = nullptr;
     CHECK(ts_issue(e, sess, &r.info, d.data(), d.size(), iteration, nullptr, &t));
+    // non-blocking ownership hand-over: the ticket frees the structured values
+    std::vector<ts_value*> owned;
+    for (auto& o : r.objs)
+      if (o.value) owned.push_back(o.value), o.value = nullptr;
+    CHECK(ts_ticket_adopt_values(t, owned.data(), owned.size()));
     // lazy contract: before mutating the state, the pre-update barrier
     int64_t blocked = 0;
     CHECK(ts_pre_update_barrier(e, t, nullptr, 1, &blocked));

@@ -1,7 +1,8 @@
 """Disk flush A/B: page-cache flush (flush_mmap=1, default) vs O_DIRECT flush
 (flush_mmap=2) of one rank's state to a disk filesystem. Reports the time to
 "persisted" (files + footers + manifest written) and to persisted + sync(2)
-(bytes on the device), per mode, alternating modes.
+(bytes on the device), per mode, alternating modes. Mode 3: O_DIRECT through
+io_uring.
 
   python tools/direct_io_bench.py [--gb 8] [--root /var/tmp] [--reps 2]
 """
@@ -67,7 +68,7 @@ def main():
             os.sync()
             t2 = time.perf_counter()
             s = t.stats()
-            print(json.dumps({"mode": {1: "page-cache", 2: "O_DIRECT"}[mode], "rep": rep, "gb": round(total / 1e9, 2),
+            print(json.dumps({"mode": {1: "page-cache", 2: "O_DIRECT", 3: "O_DIRECT+io_uring"}[mode], "rep": rep, "gb": round(total / 1e9, 2),
                               "persisted_gbps": round(total / (t1 - t0) / 1e9, 2),
                               "synced_gbps": round(total / (t2 - t0) / 1e9, 2),
                               "sync_s": round(t2 - t1, 2),
@@ -75,7 +76,7 @@ def main():
                               "workers": cfg.flush_workers, "window_mb": cfg.raw_chunk_bytes >> 20}), flush=True)
             eng.shutdown()
             if a.restore:
-                for dio, cold in ((False, True), (True, True), (None, True), (None, False)):
+                for dio, cold in ((False, True), (True, True), ("uring", True), (None, True), (None, False)):
                     dropped = drop_caches() if cold else False
                     r = api.Restorer(os.path.join(d, "MANIFEST.tlv"), direct_io=dio)
                     torch.cuda.synchronize()
@@ -84,7 +85,8 @@ def main():
                     torch.cuda.synchronize()
                     dt = time.perf_counter() - t0
                     ok = all(torch.equal(o.payload, so.payload) for o, so in zip(rs.objects, objs))
-                    print(json.dumps({"restore": {False: "pread", True: "O_DIRECT", None: "auto"}[dio],
+                    print(json.dumps({"restore": {False: "pread", True: "O_DIRECT", "uring": "O_DIRECT+io_uring",
+                                                  None: "auto"}[dio],
                                       "written_by": mode,
                                       "caches_dropped": dropped, "gbps": round(total / dt / 1e9, 2),
                                       "direct_io_frac": round(r.last_stats["direct_io_bytes"] / total, 3),
