@@ -624,7 +624,7 @@ def ours(args):
 
     # the TMA bulk kernel runs only for a full device shadow (engine.cpp run_job);
     # a multi-slot HBM ring (cfg4) packs every chunk with the warp kernel
-    pack_used = "bulk" if (shadow and args.pack_kernel == "bulk") else "warp"
+    pack_used = "bulk" if ((shadow and args.pack_kernel != "warp") or args.pack_kernel == "bulk-ring") else "warp"
     pack_label = ("copy-engine DMA" if args.mode == "direct" else
                   "pack_bulk_kernel (TMA) + pack_kernel" if pack_used == "bulk" else "pack_kernel (warp gather)")
     cpu = None
@@ -849,7 +849,7 @@ def main():
                          "cfg1, cfg1b, cfg2, cfg3")
     ap.add_argument("--mode", default="ring", choices=["ring", "direct", "zerocopy"])
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--train-steps", type=int, default=4,
+    ap.add_argument("--train-steps", type=int, default=8,
                     help="timed steps per off/lazy block (rounded up to whole checkpoint cycles)")
     ap.add_argument("--fwd-bwd-ms", type=float, default=1800.0)
     ap.add_argument("--fwd-bwd", default="graph", choices=["graph", "eager"],
@@ -861,7 +861,7 @@ def main():
     ap.add_argument("--hbm-frac", type=float, default=0.35,
                     help="share of the synthetic fwd/bwd spent in an HBM-bound elementwise phase")
     ap.add_argument("--host-checksum", action="store_true", help="FNV on host threads instead of the GPU kernels")
-    ap.add_argument("--pack-kernel", default="bulk", choices=["warp", "bulk"],
+    ap.add_argument("--pack-kernel", default="bulk", choices=["warp", "bulk", "bulk-ring"],
                     help="bulk: TMA cp.async.bulk for large 16-B aligned fragments + warp kernel for the rest")
     ap.add_argument("--ck-priority", type=int, default=-1, help="device checksum stream priority (1/0/-1)")
     ap.add_argument("--ck-host-frac", type=float, default=-1.0,

@@ -180,8 +180,10 @@ typedef struct ts_engine_config {
                                        unavailable) */
   int32_t pack_kernel;              /* RING pack: 1 (default) = TMA bulk copies (cp.async.bulk
                                        through shared memory) for 16-B aligned fragments >=
-                                       bulk_min_bytes, warp kernel for the rest; 0 = warp gather
-                                       kernel for everything */
+                                       bulk_min_bytes, warp kernel for the rest, when the whole
+                                       image fits the device staging (one pack); 2 = also in a
+                                       multi-slot ring, with a 2-stage (64 KiB) kernel; 0 = warp
+                                       gather kernel for everything */
   uint64_t bulk_min_bytes;          /* default 1 MiB */
   int32_t file_dma;                 /* 1 (default): D2H windows land directly in page-locked
                                        file pages (cudaHostRegister of a shared mapping, tmpfs)

@@ -345,6 +345,7 @@ class EngineConfig:
     checksum_on_gpu: bool = True
     flush_mmap: int = 1  # 1: copy into a shared mapping; 0: pwrite; 2: O_DIRECT body + pwrite head/tail; 3: 2 via io_uring
     pack_kernel: str = "bulk"  # "bulk" (TMA cp.async.bulk for large aligned fragments + warp kernel) | "warp"
+    #                          | "bulk-ring" (also in a multi-slot ring, 2-stage / 64 KiB kernel)
     bulk_min_bytes: int = 1 << 20
     file_dma: bool = True  # D2H straight into page-locked file pages when registered (rotation)
     checksum_priority: int = -1  # RING device checksums' stream: 1 high, 0 normal, -1 low (default)
@@ -376,7 +377,7 @@ class EngineConfig:
         c.write_files = int(self.write_files)
         c.checksum_on_gpu = int(self.checksum_on_gpu)
         c.flush_mmap = int(self.flush_mmap)
-        c.pack_kernel = {"warp": 0, "bulk": 1}[self.pack_kernel]
+        c.pack_kernel = {"warp": 0, "bulk": 1, "bulk-ring": 2}[self.pack_kernel]
         c.bulk_min_bytes = self.bulk_min_bytes
         c.file_dma = int(self.file_dma)
         c.checksum_priority = int(self.checksum_priority)

@@ -932,7 +932,7 @@ void engine::run_job(const std::shared_ptr<job>& j) {
   uint8_t* ring = nullptr;
   if (mode == TS_D2H_RING && j->img > 0) {
     // (a whole number of bulk jobs, so the TMA path can run on a full shadow too)
-    const uint64_t want = align_up(j->img, cfg_.pack_kernel == 1 ? static_cast<uint64_t>(dev::kBulkJob) : 256);
+    const uint64_t want = align_up(j->img, cfg_.pack_kernel >= 1 ? static_cast<uint64_t>(dev::kBulkJob) : 256);
     const uint64_t cap = std::max<uint64_t>(cfg_.device_staging_bytes, 2 * W);
     if (cap >= want) {
       chunk = want;
@@ -963,7 +963,11 @@ void engine::run_job(const std::shared_ptr<job>& j) {
   // slots every chunk's pack is issued while training kernels run, and the
   // bulk kernel's CTAs (192 KiB of shared memory each) then wait for whole SMs
   // — measured: cfg4 with a ring, 22 % step slowdown with bulk vs 4 % warp.
-  if (use_ring && nslots == 1 && cfg_.pack_kernel == 1 && chunk % dev::kBulkJob == 0) {
+  // pack_kernel = 2 keeps the bulk path in a multi-slot ring with a 2-stage
+  // (64 KiB) kernel, small enough to share an SM with training CTAs that leave
+  // 64 KiB of shared memory free.
+  const bool bulk_ring = cfg_.pack_kernel == 2 && nslots > 1;
+  if (use_ring && ((nslots == 1 && cfg_.pack_kernel >= 1) || bulk_ring) && chunk % dev::kBulkJob == 0) {
     for (const auto& sg : j->segs) {
       const uint64_t body = sg.len & ~15ull;
       const bool bulk = sg.src && (reinterpret_cast<uintptr_t>(sg.src) & 15) == 0 && (sg.pos & 15) == 0 &&
@@ -1119,8 +1123,8 @@ void engine::run_job(const std::shared_ptr<job>& j) {
                                    [](const dev::bulk_job& b, uint64_t x) { return b.pos < x; });
         auto ub = std::lower_bound(lb, bjobs.end(), chi, [](const dev::bulk_job& b, uint64_t x) { return b.pos < x; });
         if (ub > lb) {
-          dev::launch_pack_bulk(d_jobs + (lb - bjobs.begin()), static_cast<uint32_t>(ub - lb), clo, slot, sms_,
-                                pack_stream_);
+          dev::launch_pack_bulk(d_jobs + (lb - bjobs.begin()), static_cast<uint32_t>(ub - lb), clo, slot,
+                                bulk_ring ? 3 * sms_ : sms_, pack_stream_, bulk_ring ? 2 : 6);
           t.kernel_launches += 1;
         }
       }

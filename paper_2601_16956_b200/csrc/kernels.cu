@@ -273,12 +273,15 @@ __global__ void __launch_bounds__(512) pattern_kernel(const pseg* __restrict__ s
 // ---------------------------------------------------------------------------
 // Bulk copy through shared memory with the TMA engine (cp.async.bulk).
 
-constexpr int kBulkStages = 6;  // 6 x 32 KiB = 192 KiB of shared memory per CTA
+// Stages of 32 KiB: 6 (192 KiB of shared memory per CTA) for a full-shadow
+// pack that owns the GPU; 2 (64 KiB) for ring slots packed while training
+// kernels hold most of every SM's shared memory.
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+template <int kBulkStages>
 __global__ void __launch_bounds__(32) pack_bulk_kernel(const bulk_job* __restrict__ jobs, uint32_t njobs,
                                                        uint64_t lo, uint8_t* dst) {
   extern __shared__ __align__(128) uint8_t stage_buf[];
@@ -355,21 +358,24 @@ void launch_pack(const seg* d_segs, uint32_t nsegs, uint64_t lo, uint64_t hi, ui
 }
 
 void launch_pack_bulk(const bulk_job* d_jobs, uint32_t njobs, uint64_t lo, uint8_t* dst, int ctas,
-                      cudaStream_t st) {
+                      cudaStream_t st, int stages) {
   if (njobs == 0) return;
-  // The dynamic shared memory opt-in is per device: one process may drive
-  // engines (or helper streams) on several GPUs.
-  static std::atomic<uint64_t> attr_set{0};
-  const int smem = kBulkStages * static_cast<int>(kBulkJob);
+  // The dynamic shared memory opt-in is per device (and per instantiation):
+  // one process may drive engines (or helper streams) on several GPUs.
+  static std::atomic<uint64_t> attr_set[2] = {{0}, {0}};
+  const bool few = stages <= 2;
+  const int smem = (few ? 2 : 6) * static_cast<int>(kBulkJob);
   int dev = 0;
   cudaGetDevice(&dev);
   const uint64_t bit = 1ull << (dev & 63);
-  if (!(attr_set.load() & bit)) {
-    cudaFuncSetAttribute(pack_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_set.fetch_or(bit);
+  if (!(attr_set[few].load() & bit)) {
+    if (few) cudaFuncSetAttribute(pack_bulk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    else cudaFuncSetAttribute(pack_bulk_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_set[few].fetch_or(bit);
   }
   const int grid = static_cast<int>(std::min<uint64_t>(njobs, static_cast<uint64_t>(ctas)));
-  pack_bulk_kernel<<<grid, 32, smem, st>>>(d_jobs, njobs, lo, dst);
+  if (few) pack_bulk_kernel<2><<<grid, 32, smem, st>>>(d_jobs, njobs, lo, dst);
+  else pack_bulk_kernel<6><<<grid, 32, smem, st>>>(d_jobs, njobs, lo, dst);
   count_launch();
 }
 

@@ -59,7 +59,7 @@ struct bulk_job {
 };
 // Copies jobs whose pos lies in [lo, hi) into dst (dst[0] = image byte lo).
 void launch_pack_bulk(const bulk_job* d_jobs, uint32_t njobs, uint64_t lo, uint8_t* dst, int ctas,
-                      cudaStream_t st);
+                      cudaStream_t st, int stages = 6);
 
 // Scatter-unpack: image bytes [lo, hi) held in src (src[0] = image byte lo)
 // to the destination pieces that intersect the range.

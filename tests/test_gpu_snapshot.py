@@ -264,3 +264,22 @@ def test_bulk_path_engaged_on_shadow(gpu, tmp_path, name):
         launches[label] = sum(s["kernel_launches"] for s in stats)
     ranks_with_big = sum(1 for r in rec.ranks if any(o.kind == 0 and o.tier == 0 and o.size >= 32768 for o in r.objects))
     assert launches["bulk"] == launches["warp"] + ranks_with_big
+
+
+@pytest.mark.parametrize("name", ["hand_mixed", "odd_layout", "tiny_layout", "nozero_dp2"])
+def test_bulk_ring_two_stage_kernel(gpu, tmp_path, name):
+    """pack_kernel="bulk-ring": the 2-stage (64 KiB shared memory) TMA bulk
+    kernel also runs in a multi-slot HBM ring (one launch per ring chunk that
+    holds bulk jobs); the bytes stay identical to the reference's."""
+    rec = S.load_recipe(os.path.join(GOLDEN, "recipes", name + ".recipe"))
+    launches = {}
+    for label, pk in (("warp", "warp"), ("bulk-ring", "bulk-ring")):
+        out = str(tmp_path / label)
+        # windows of 64 KiB (2 bulk jobs), a 4-window ring: many chunks per rank
+        _, _, stats, _ = checkpoint_recipe(rec, out, cfg_for("ring", pack_kernel=pk, bulk_min_bytes=32768,
+                                                             raw_chunk_bytes=64 << 10, device_staging_bytes=256 << 10))
+        assert read_tree(out) == read_tree(os.path.join(GOLDEN, "trees", name))
+        launches[label] = sum(s["kernel_launches"] for s in stats)
+    big = any(o.kind == 0 and o.tier == 0 and o.size >= 65536 for r in rec.ranks for o in r.objects)
+    if big:
+        assert launches["bulk-ring"] > launches["warp"]
