@@ -91,16 +91,18 @@ class Clocks:
 
 
 def ncu_traffic(cfg: str, mode: str, pack_kernel: str):
-    """DRAM bytes per pack launch from the committed ncu --set full capture of
-    this workload (profiles/ncu_traffic.json), else None."""
+    """DRAM bytes of the pack kernels of one checkpoint of this workload from
+    the committed ncu capture (profiles/ncu_traffic.json: cfg2 full-shadow
+    bulk+warp, cfg4 ring warp), else None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             t = json.load(f)
     except Exception:
         return None
-    if t.get("workload") != cfg or mode != "ring" or pack_kernel != t.get("pack_kernel", "warp"):
-        return None
-    return int(t["traffic_bytes_per_launch"])
+    for e in t.get("entries", [t]):
+        if e.get("workload") == cfg and mode == "ring" and pack_kernel == e.get("pack_kernel", "warp"):
+            return int(e["traffic_bytes_per_launch"])
+    return None
 
 
 def pcie_d2h_peak(dev) -> float:
@@ -889,7 +891,7 @@ def main():
     ap.add_argument("--ring-gb", type=float, default=0.0,
                     help="HBM staging ring when no full device shadow fits (0 = auto: free HBM - 26 GiB)")
     ap.add_argument("--ring-chunk-gb", type=float, default=0.0, help="ring slot size (0 = auto)")
-    ap.add_argument("--worker-nice", type=int, default=10, help="nice increment of engine worker threads")
+    ap.add_argument("--worker-nice", type=int, default=19, help="nice increment of engine worker threads")
     ap.add_argument("--no-balance", dest="balance", action="store_false",
                     help="N>1: no D2H load balancing onto helper GPUs")
     args = ap.parse_args()

@@ -203,7 +203,7 @@ typedef struct ts_engine_config {
                                        ring/6, at most 8 GiB; rounded to whole windows) */
   int32_t numa_bind;                /* 1 (default): engine threads and the pinned pool on the GPU's
                                        NUMA node (multi-socket hosts; no-op on one node) */
-  int32_t worker_nice;              /* nice increment of the worker threads (default 10: background
+  int32_t worker_nice;              /* nice increment of the worker threads (default 19: background
                                        to the training process's launching thread); 0 = none */
   uint32_t helper_mask;             /* RING: devices (bit i = device i) whose copy engines may carry
                                        part of this rank's D2H, reading the staged image over NVLink

@@ -352,7 +352,7 @@ class EngineConfig:
     checksum_host_frac: float = -1.0  # share hashed by host workers: 0 all GPU, <0 auto (default)
     ring_chunk_bytes: int = 0  # RING slot size without a full shadow (0 = auto: ring/6, <= 8 GiB)
     numa_bind: bool = True  # engine threads + pinned pool on the GPU's NUMA node (multi-socket hosts)
-    worker_nice: int = 10  # nice increment of the background worker threads (0 = none)
+    worker_nice: int = 19  # nice increment of the background worker threads (0 = none)
     helper_devices: tuple = ()  # RING: GPUs whose copy engines carry part of this rank's D2H (NVLink read)
     helper_share: float = 0.0  # fraction of the image they carry
 

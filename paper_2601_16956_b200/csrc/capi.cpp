@@ -203,7 +203,7 @@ void ts_engine_config_default(ts_engine_config* c) {
   c->checksum_host_frac = -1.0;
   c->ring_chunk_bytes = 0;
   c->numa_bind = 1;
-  c->worker_nice = 10;
+  c->worker_nice = 19;
   c->helper_mask = 0;
   c->helper_share = 0.0;
 }

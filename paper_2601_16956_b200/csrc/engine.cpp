@@ -691,7 +691,11 @@ void engine::prepare(const std::shared_ptr<job>& j, const ts_rank_info& rank, co
       // no slack) keeps everything on the GPU, so host-held pool windows can
       // never throttle the D2H. One host chain must finish within D2H + slack.
       const double d2h_s = static_cast<double>(j->img) / 50e9;
-      frac = dev_bytes ? std::min(1.0, 0.8 * host_rate_ * slack_s_ / static_cast<double>(dev_bytes)) : 0.0;
+      // (experiment knob TS_HOST_CK_D2H=1: the host may also use the D2H time
+      // itself when there is slack, i.e. a training loop)
+      static const bool with_d2h = std::getenv("TS_HOST_CK_D2H") != nullptr;
+      const double budget = slack_s_ + (with_d2h && slack_s_ > 0 ? d2h_s : 0.0);
+      frac = dev_bytes ? std::min(1.0, 0.8 * host_rate_ * budget / static_cast<double>(dev_bytes)) : 0.0;
       obj_cap = 0.8 * chain_rate_ * (d2h_s + slack_s_);
       // Host-hashed windows that land in the pinned pool hold it until hashed:
       // only when the pool takes all of them can hashing not throttle the D2H.
