@@ -765,8 +765,10 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0, snap_ms):
             comp.synchronize()  # like a per-step loss.item(): the compute stream only, never the device
             t0 = time.perf_counter()
             ev0.record(comp)
+            t_rec = time.perf_counter()
             run()                                    # forward + backward
             ev1.record(comp)
+            t_launch = time.perf_counter()
             comp.synchronize()  # fwd/bwd done (the simulator's synchronous phases, simulator.cpp:129-130)
             if k > 0:
                 fb_gpu[mode].append(ev0.elapsed_time(ev1))
@@ -797,7 +799,8 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0, snap_ms):
             if k > 0:
                 p_end = time.perf_counter()
                 times.append(p_end - t0)
-                phases[mode].append((p_fb - t0, p_bar - p_fb, p_upd - p_bar, p_iss - p_upd, p_end - p_iss))
+                phases[mode].append((p_fb - t0, t_rec - t0, t_launch - t_rec, p_bar - p_fb, p_upd - p_bar,
+                                     p_iss - p_upd, p_end - p_iss))
                 if mode == "lazy" and k % interval == 0:
                     blocked.append(1e3 * (b / 1e9 + ib))
                 elif b and blocked:
@@ -831,9 +834,15 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0, snap_ms):
             "issue_ms": {"engine": round(statistics.mean(issue_cpp), 3) if issue_cpp else None,
                          "python_call": round(statistics.mean(issue_py), 3) if issue_py else None},
             "fwd_bwd_gpu_ms": {m: round(statistics.mean(v), 1) for m, v in fb_gpu.items() if v},
-            "phase_ms": {m: dict(zip(["fwd_bwd", "barrier", "update_launch", "issue", "final_sync"],
+            "phase_ms": {m: dict(zip(["fwd_bwd", "fwd_bwd_event_record", "fwd_bwd_launch", "barrier", "update_launch",
+                                      "issue", "final_sync"],
                                      [round(1e3 * statistics.mean(x), 2) for x in zip(*v)]))
                          for m, v in phases.items() if v},
+            "phase_ms_max": {m: dict(zip(["fwd_bwd", "fwd_bwd_event_record", "fwd_bwd_launch", "barrier",
+                                          "update_launch", "issue", "final_sync"],
+                                         [round(1e3 * max(x), 2) for x in zip(*v)]))
+                             for m, v in phases.items() if v},
+            "fwd_bwd_gpu_ms_max": {m: round(max(v), 1) for m, v in fb_gpu.items() if v},
             "clocks": {m: {"sm_mhz": [c["sm_mhz"] for c in v], "power_w": [c.get("power_w") for c in v],
                            "reasons": sorted({r for c in v for r in c["reasons"]})} for m, v in clk.items()},
             "checkpoints_to": (f"files on /dev/shm, rotation keeps {args.keep}, file_dma bytes of the last "
