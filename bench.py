@@ -596,6 +596,10 @@ def ours(args):
         rs.seed = spec.seed
         bad = api.pattern_mismatches(rs, it)
         e2e["restore_gbps"] = round(raw / restore_s / 1e9, 3)
+        e2e["restore_what"] = ("restore_gbps: files in the page cache but not page-locked by this process "
+                               "(a restart: pread -> pinned ring -> H2D -> unpack; bound by the host's copy "
+                               "bandwidth); restore_warm_gbps: files this process page-locked through "
+                               "rotation (H2D straight from the page cache)")
         e2e["restore_warm_gbps"] = round(raw / restore_warm_s / 1e9, 3)
         e2e["restore_warm_direct_bytes"] = int(r3.last_stats.get("direct_bytes", 0))
         e2e["restore_bit_exact"] = bad == 0 and bad_cold == 0
