@@ -681,6 +681,13 @@ def ours(args):
         dist.destroy_process_group()
 
 
+def auto_interval(snapshot_ms: float, step_ms: float) -> int:
+    """The most frequent checkpoint cadence (in steps) the D2H link sustains:
+    one snapshot, with 10 % margin, must fit into the steps between two
+    checkpoints."""
+    return max(1, math.ceil(1.1 * snapshot_ms / max(step_ms, 1e-9)))
+
+
 def training_phase(args, api, state, spec, cfg, local, dev, it0, snap_ms):
     """fwd+bwd (bf16 GEMMs) -> pre_update_barrier -> update -> issue, with and
     without checkpointing; reports host-blocked ms per checkpoint (issue_block +
@@ -692,7 +699,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0, snap_ms):
     # the D2H link sustains: a snapshot (measured above) must fit, with 10 %
     # margin, into the steps between two checkpoints. A 120.7 GB shard over one
     # PCIe Gen5 x16 link takes ~2.2 s, longer than a 1.8 s step: every 2 steps.
-    interval = args.ckpt_interval or max(1, math.ceil(1.1 * snap_ms / fb_ms))
+    interval = args.ckpt_interval or auto_interval(snap_ms, fb_ms)
     n_steps = -(-args.train_steps // interval) * interval  # whole checkpoint cycles per timed block
     # Long-lived objects (thousands of state descriptors) out of the cyclic GC's
     # reach, as training loops do: a full collection over them landed inside
