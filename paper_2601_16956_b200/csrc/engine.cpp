@@ -44,6 +44,7 @@ void mkdirs(const std::string& path) {
 
 namespace {
 const bool g_trace = std::getenv("TS_TRACE") != nullptr;
+const bool g_trace_copies = std::getenv("TS_TRACE_COPIES") != nullptr;  // per-job enqueue cost summary
 #define TRACE(...)                                                                     \
   do {                                                                                 \
     if (g_trace) {                                                                     \
@@ -204,6 +205,7 @@ struct job {
 
   std::mutex mu;
   size_t wins_landed = 0, wins_enqueued = 0, structs_pending = 0, files_done = 0;
+  std::condition_variable land_cv;  // wins_landed advanced (bounded enqueue in run_job)
   bool enqueue_done = false, snapshot_done = false, persisted = false;
 };
 
@@ -925,6 +927,24 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     std::lock_guard<std::mutex> g(t.mu);
     return t.failed;
   };
+  // Bounded enqueue: at most `max_inflight` windows between enqueue and
+  // landing (~8 GiB, 8-256 windows). An unbounded burst of copies fills the
+  // copy stream's queue, after which every cudaMemcpyAsync blocks inside the
+  // driver for a window's transfer time — and the training thread's own CUDA
+  // calls (event records, graph launches) stall behind it (measured: 35 ms
+  // mean, up to 494 ms per call on cfg4). Waiting here instead keeps the
+  // driver free.
+  const size_t max_inflight = std::clamp<size_t>(
+      static_cast<size_t>((8ull << 30) / std::max<uint64_t>(j->win_bytes, 1)), 8, 256);
+  auto throttle = [&] {
+    std::unique_lock<std::mutex> g(j->mu);
+    while (j->wins_enqueued >= j->wins_landed + max_inflight) {
+      g.unlock();
+      if (failed()) return;
+      g.lock();
+      j->land_cv.wait_for(g, std::chrono::milliseconds(20));
+    }
+  };
 
   // Device staging plan (RING): the whole image when it fits (device shadow);
   // else a ring of `nslots` chunks of whole windows (>= 1 GiB each when the
@@ -1061,6 +1081,14 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     j->fnv_out = ck_host_;
     j->fnv_ev = get_event();
   }
+  bool fnv_publish = false;
+  auto publish_fnv = [&] {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      inflight_.push_back({j, 0, true});
+    }
+    cv_.notify_all();
+  };
   // Launch k of the checksum kernels; the last one publishes the results
   // straight into the mapped pool region (a cudaMemcpy would queue behind the
   // bulk D2H windows on the copy engine).
@@ -1081,11 +1109,11 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     if (k + 2 != cbeg.size()) return;
   publish:
     cuda_check(cudaEventRecord(j->fnv_ev, cs), "event");
-    {
-      std::lock_guard<std::mutex> g(mu_);
-      inflight_.push_back({j, 0, true});
-    }
-    cv_.notify_all();
+    // RING: the completer learns about the results only after the last
+    // window, so it never blocks on the checksums ahead of windows whose
+    // landing the bounded enqueue is waiting for
+    if (use_ring) fnv_publish = true;
+    else publish_fnv();
   };
   cuda_check(cudaStreamWaitEvent(pack_stream_, t.ev_start, 0), "wait producer");
   cuda_check(cudaStreamWaitEvent(copy_stream_, t.ev_start, 0), "wait producer");
@@ -1103,13 +1131,27 @@ void engine::run_job(const std::shared_ptr<job>& j) {
 
   if (mode == TS_D2H_RING) {
     const bool shadow = nslots == 1;
+    int64_t copy_call_ns = 0, copy_call_max_ns = 0;
+    const int64_t t_enqueue0 = now_ns();
     j->chunk_events.assign(nchunks, nullptr);
     j->ck_events.assign(nchunks, nullptr);
     uint64_t seen_bytes = 0, helper_done = 0;
     size_t helper_next = 0;
-    size_t w = 0;
+    // Windows of each chunk, in D2H order: [cw0[c], cw0[c + 1]) (a shadow is one chunk).
+    std::vector<size_t> cw0(nchunks + 1, j->wins.size());
+    for (size_t c = 0, q = 0; c < nchunks; ++c) {
+      cw0[c] = q;
+      const uint64_t chi = std::min(j->img, (c + 1) * chunk);
+      while (q < j->wins.size() && (shadow || j->wins[q].lo < chi)) ++q;
+    }
+    std::vector<cudaEvent_t> packed_ev(nchunks, nullptr);
     cuda_check(cudaEventRecord(t.ev_d2h_first, copy_stream_), "event");
-    for (size_t c = 0; c < nchunks && !failed(); ++c) {
+
+    // Pack of chunk c (+ its host-tier bytes and device checksums). Enqueued as
+    // soon as the slot's previous chunk has its D2H and checksums enqueued, so
+    // packs run up to a ring-full ahead of the window copies; the GPU-side
+    // waits order them after the slot is free.
+    auto enqueue_pack = [&](size_t c) {
       const uint64_t clo = c * chunk, chi = std::min(j->img, clo + chunk);
       uint8_t* slot = ring + (shadow ? 0 : (c % nslots) * chunk);
       if (c >= nslots) {  // the slot's previous chunk must have left the device and been checksummed
@@ -1137,22 +1179,16 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       // Host-tier bytes join the staged image in stream order, before the
       // capture event: the pre-update barrier then covers them too (copying
       // them at window landing, after the barrier, let an update leak in).
-      for (size_t q = w; q < j->wins.size() && j->wins[q].lo < chi; ++q) {
+      for (size_t q = cw0[c]; q < cw0[c + 1]; ++q) {
         const auto& wq = j->wins[shadow ? j->worder[q] : q];
         for (uint32_t k = wq.hp_begin; k < wq.hp_end; ++k)
           cuda_check(cudaMemcpyAsync(slot + (wq.lo + j->hp[k].win_off - clo), j->hp[k].src, j->hp[k].len,
                                      cudaMemcpyHostToDevice, pack_stream_), "host-tier bytes to the staged image");
       }
       cuda_check(cudaGetLastError(), "pack kernel launch");
-      cudaEvent_t packed;
-      cuda_check(cudaEventCreateWithFlags(&packed, cudaEventDisableTiming), "event");
-      cuda_check(cudaEventRecord(packed, pack_stream_), "event");
+      cuda_check(cudaEventCreateWithFlags(&packed_ev[c], cudaEventDisableTiming), "event");
+      cuda_check(cudaEventRecord(packed_ev[c], pack_stream_), "event");
       if (c + 1 == nchunks) mark_capture(pack_stream_);
-      cuda_check(cudaStreamWaitEvent(copy_stream_, packed, 0), "wait pack");
-      struct ev_guard {  // destruction is deferred until the event completes
-        cudaEvent_t e;
-        ~ev_guard() { cudaEventDestroy(e); }
-      } packed_guard{packed};
       if (nf) {  // reads the slot on the checksum stream, overlapping the D2H
         // chunks whose slot is packed again in this job: capture path, pack
         // priority; the last ring-full: low priority (chained states keep the
@@ -1166,17 +1202,27 @@ void engine::run_job(const std::shared_ptr<job>& j) {
           cuda_check(cudaStreamWaitEvent(ck_stream_, hand, 0), "checksum order");
           cudaEventDestroy(hand);
         }
-        cuda_check(cudaStreamWaitEvent(cs, packed, 0), "wait pack");
+        cuda_check(cudaStreamWaitEvent(cs, packed_ev[c], 0), "wait pack");
         launch_checksums(c, cs);
         cudaEvent_t ck;
         cuda_check(cudaEventCreateWithFlags(&ck, cudaEventDisableTiming), "event");
         cuda_check(cudaEventRecord(ck, cs), "event");
         j->ck_events[c] = ck;
       }
+    };
+
+    size_t next_pack = 0;
+    for (size_t c = 0; c < nchunks && !failed(); ++c) {
+      while (next_pack < nchunks && (next_pack < nslots || j->chunk_events[next_pack - nslots] != nullptr))
+        enqueue_pack(next_pack++);
+      const uint64_t clo = c * chunk;
+      uint8_t* slot = ring + (shadow ? 0 : (c % nslots) * chunk);
+      cuda_check(cudaStreamWaitEvent(copy_stream_, packed_ev[c], 0), "wait pack");
       std::vector<char> helper_used(helpers_.size(), 0);
-      for (size_t q = w; q < j->wins.size() && j->wins[q].lo < chi; ++q, ++w) {
+      for (size_t q = cw0[c]; q < cw0[c + 1]; ++q) {
         const size_t wi = shadow ? j->worder[q] : q;
         auto& win = j->wins[wi];
+        throttle();
         acquire(win);
         const uint64_t len = win.hi - win.lo;
         cudaStream_t cs = copy_stream_;
@@ -1189,14 +1235,20 @@ void engine::run_job(const std::shared_ptr<job>& j) {
           win.helper = static_cast<int>(k);
           cs = helpers_[k]->st;
           if (!helper_used[k]) {  // once per chunk: the helper copies only after the pack
-            cuda_check(cudaStreamWaitEvent(cs, packed, 0), "helper waits for the pack");
+            cuda_check(cudaStreamWaitEvent(cs, packed_ev[c], 0), "helper waits for the pack");
             helper_used[k] = 1;
           }
           helper_done += len;
           t.helper_bytes += len;
         }
         seen_bytes += len;
+        const int64_t tc0 = now_ns();
         const cudaError_t ce = cudaMemcpyAsync(win.host, slot + (win.lo - clo), len, cudaMemcpyDeviceToHost, cs);
+        {
+          const int64_t dt = now_ns() - tc0;
+          copy_call_ns += dt;
+          copy_call_max_ns = std::max<int64_t>(copy_call_max_ns, dt);
+        }
         if (ce != cudaSuccess) {
           char m[256];
           std::snprintf(m, sizeof m, "D2H window [%llu, %llu) of chunk %zu at %llu (ring %llu B, host %p dma %d)",
@@ -1221,7 +1273,14 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       cuda_check(cudaEventRecord(done, copy_stream_), "event");
       j->chunk_events[c] = done;
     }
+    for (auto& e : packed_ev)  // (destruction is deferred until each event completes)
+      if (e) cudaEventDestroy(e);
+    if (fnv_publish) publish_fnv();
     cuda_check(cudaEventRecord(t.ev_d2h_last, copy_stream_), "event");
+    if (g_trace_copies)
+      std::fprintf(stderr, "[ts] run_job rank=%d windows=%zu: host time in cudaMemcpyAsync %.1f ms (max %.2f ms), "
+                   "whole enqueue %.1f ms\n", j->rank_id, j->wins.size(), copy_call_ns / 1e6, copy_call_max_ns / 1e6,
+                   (now_ns() - t_enqueue0) / 1e6);
     // later jobs reuse the ring and the checksum scratch: order them after these checksums
     if (nf) {
       cudaEvent_t tail;
@@ -1238,6 +1297,7 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     for (size_t q = 0; q < j->wins.size() && !failed(); ++q) {
       const size_t w = j->worder[q];
       auto& win = j->wins[w];
+      throttle();
       acquire(win);
       uint8_t* dst = nullptr;  // device view of the mapped pool region / locked file pages
       if (win.dma) {
@@ -1263,6 +1323,7 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     for (size_t q = 0; q < j->wins.size() && !failed(); ++q) {
       const size_t w = j->worder[q];
       auto& win = j->wins[w];
+      throttle();
       acquire(win);
       uint8_t* dst = win.host;
       size_t k = std::upper_bound(j->segs.begin(), j->segs.end(), win.lo,
@@ -1328,6 +1389,7 @@ void engine::completer_loop() {
         std::lock_guard<std::mutex> g(j->mu);
         j->wins_landed += 1;
       }
+      j->land_cv.notify_all();
       if (!win.dma) pool_->release(win.r);
       continue;
     }
@@ -1368,6 +1430,7 @@ void engine::window_landed(const std::shared_ptr<job>& j, size_t wi) {
     j->wins_landed += 1;
     release_now = w.refs == 0;
   }
+  j->land_cv.notify_all();
   if (release_now && !w.dma) pool_->release(w.r);
   bool last;
   {

@@ -283,3 +283,25 @@ def test_bulk_ring_two_stage_kernel(gpu, tmp_path, name):
     big = any(o.kind == 0 and o.tier == 0 and o.size >= 65536 for r in rec.ranks for o in r.objects)
     if big:
         assert launches["bulk-ring"] > launches["warp"]
+
+
+@pytest.mark.parametrize("mode", ["ring", "direct", "zerocopy"])
+def test_bounded_enqueue_many_windows(gpu, tmp_path, mode):
+    """~1,300 windows of 64 KiB (the copier keeps at most 256 in flight and
+    packs run a ring-full ahead of the copies): bytes and checksums intact."""
+    n = (80 << 20) + 12345
+    x = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda")
+    eng = api.CheckpointEngine(api.EngineConfig(d2h_mode=mode, raw_chunk_bytes=64 << 10, staging_capacity_bytes=8 << 20,
+                                                device_staging_bytes=2 << 20, flush_workers=3), 0, 0)
+    sess = api.CheckpointSession(str(tmp_path / "c"), 1, 1, None, n_ranks=1)
+    st = api.RankState(objects=[api.StateObject(1, size_bytes=n, payload=x),
+                                api.StateObject(2, kind=api.KIND_STRUCTURED, residency=api.TIER_HOST, file_id=0,
+                                                structured={"n": n})])
+    t = eng.issue_checkpoint(sess, st, 1)
+    eng.pre_update_barrier(t)
+    t.wait_persisted()
+    sess.wait_complete(60)
+    assert t.object_checksum(1) == api.fnv1a64(x.cpu().numpy().tobytes())
+    eng.shutdown()
+    rs = api.restore_checkpoint(str(tmp_path / "c" / "MANIFEST.tlv"))
+    assert torch.equal(rs[0].objects[0].payload.cuda(), x)
