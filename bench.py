@@ -734,6 +734,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0, snap_ms):
     comp = torch.cuda.current_stream()
     res = {"off": ([], []), "lazy": ([], [])}
     host_ck, ck_tickets = [], []
+    page_lock = {}  # file-registry page-lock activity inside the timed blocks (holds the driver)
     issue_cpp, issue_py = [], []  # issue time inside the engine vs the whole Python call
     clk = {"off": [], "lazy": []}
     fb_gpu = {"off": [], "lazy": []}  # CUDA-event time of fwd+bwd on the compute stream
@@ -772,6 +773,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0, snap_ms):
         times, blocked = res[mode]
         sampler = Clocks(local)
         sampler.__enter__()
+        fc0 = api.file_cache_stats()
         for k in range(n_steps + 1):
             comp.synchronize()  # like a per-step loss.item(): the compute stream only, never the device
             t0 = time.perf_counter()
@@ -818,6 +820,13 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0, snap_ms):
                     blocked[-1] += 1e3 * b / 1e9  # barrier wait attributed to its checkpoint
         sampler.__exit__()
         clk[mode].append(sampler.summary())
+        fc1 = api.file_cache_stats()
+        pl = page_lock.setdefault(mode, {"registrations": 0, "register_ms": 0.0, "unregistrations": 0,
+                                         "unregister_ms": 0.0})
+        pl["registrations"] += fc1["registrations"] - fc0["registrations"]
+        pl["register_ms"] += (fc1["register_ns"] - fc0["register_ns"]) / 1e6
+        pl["unregistrations"] += fc1["unregistrations"] - fc0["unregistrations"]
+        pl["unregister_ms"] += (fc1["unregister_ns"] - fc0["unregister_ns"]) / 1e6
         if pending:
             pending.wait_persisted()
         for tk in ck_tickets:
@@ -854,6 +863,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0, snap_ms):
                                          [round(1e3 * max(x), 2) for x in zip(*v)]))
                              for m, v in phases.items() if v},
             "fwd_bwd_gpu_ms_max": {m: round(max(v), 1) for m, v in fb_gpu.items() if v},
+            "page_lock_in_blocks": {m: {k: round(v, 1) for k, v in d.items()} for m, d in page_lock.items()},
             "clocks": {m: {"sm_mhz": [c["sm_mhz"] for c in v], "power_w": [c.get("power_w") for c in v],
                            "reasons": sorted({r for c in v for r in c["reasons"]})} for m, v in clk.items()},
             "checkpoints_to": (f"files on /dev/shm, rotation keeps {args.keep}, file_dma bytes of the last "

@@ -251,6 +251,11 @@ ts_status ts_engine_provision_spares(ts_engine* e, const char* spare_dir, const 
  * locked, and an explicit release of every idle registration (files of deleted
  * checkpoints are also released at the next issue). */
 uint64_t ts_file_cache_bytes(void);
+/* Page-lock activity since process start: [registrations, ns inside
+ * cudaHostRegister, bytes registered, unregistrations, ns unregistering].
+ * Page-locking holds the driver for seconds per 100 GB; a training loop
+ * should see none of it after its rotation is warm. B200-side addition. */
+void ts_file_cache_stats(uint64_t out[5]);
 ts_status ts_file_cache_release_all(uint64_t* released_bytes);
 
 /* checkpoint_session (engine.hpp:57-90). `writes_manifest` = 1 on the process that

@@ -217,6 +217,7 @@ _sig("ts_ticket_object_checksum", i32, P, u64, C.POINTER(u64))
 _sig("ts_ticket_release", None, P)
 _sig("ts_ticket_adopt_values", i32, P, C.POINTER(P), C.c_size_t)
 _sig("ts_io_uring_available", i32)
+_sig("ts_file_cache_stats", None, C.POINTER(u64))
 _sig("ts_io_uring_ops", u64)
 _sig("ts_restore_open", i32, C.c_char_p, C.POINTER(P))
 _sig("ts_restore_close", None, P)

@@ -682,6 +682,14 @@ def file_cache_bytes() -> int:
     return int(N.lib.ts_file_cache_bytes())
 
 
+def file_cache_stats() -> Dict[str, int]:
+    """Page-lock activity of the file registry since process start."""
+    out = (C.c_uint64 * 5)()
+    N.lib.ts_file_cache_stats(out)
+    return {"registrations": out[0], "register_ns": out[1], "registered_bytes": out[2],
+            "unregistrations": out[3], "unregister_ns": out[4]}
+
+
 def file_cache_release_all() -> int:
     """Unlock every idle page-locked checkpoint file; returns the bytes released."""
     b = C.c_uint64(0)

@@ -233,6 +233,7 @@ ts_status ts_engine_set_spare_dir(ts_engine* e, const char* spare_dir) {
 }
 
 uint64_t ts_file_cache_bytes(void) { return file_registry::get().registered_bytes(); }
+void ts_file_cache_stats(uint64_t out[5]) { file_registry::get().stats(out); }
 
 ts_status ts_file_cache_release_all(uint64_t* released_bytes) {
   return guard([&] {

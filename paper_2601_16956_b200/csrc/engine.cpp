@@ -206,6 +206,12 @@ struct job {
   std::mutex mu;
   size_t wins_landed = 0, wins_enqueued = 0, structs_pending = 0, files_done = 0;
   std::condition_variable land_cv;  // wins_landed advanced (bounded enqueue in run_job)
+  int64_t t_landed_all = -1;        // now_ns() when the last window landed (the D2H's end)
+  // checksum placement inputs, taken at issue (engine::issue) for prepare
+  double slack_s = 0, slack_d2h_s = 0, host_rate = 0;
+  // host workers hash only once the whole image has landed (no competition
+  // with the D2H for host memory bandwidth; every host object's chain ready)
+  bool defer_hash = false;
   bool enqueue_done = false, snapshot_done = false, persisted = false;
 };
 
@@ -492,15 +498,23 @@ std::shared_ptr<ticket_state> engine::issue(const std::shared_ptr<session>& sp, 
     // persist to this issue (EMA). ~0 when the caller waits for persist before
     // issuing again (closed loop), large when checkpoints are spaced by
     // training steps; forgotten after a long pause.
-    int64_t prev_issue = 0, prev_persist = -1;
+    int64_t prev_issue = 0, prev_persist = -1, prev_landed = -1;
     {
       std::lock_guard<std::mutex> g(last_job_->t->mu);
       prev_issue = last_job_->t->t_issue;
       prev_persist = last_job_->t->persisted ? last_job_->t->t_persisted : -1;
     }
+    {
+      std::lock_guard<std::mutex> g(last_job_->mu);
+      prev_landed = last_job_->t_landed_all;
+    }
     const double gap = prev_persist < 0 ? 0.0 : static_cast<double>(t0 - prev_issue - prev_persist) / 1e9;
     // (drops at once when the host fell behind, grows slowly)
     slack_s_ = gap > 120 ? 0 : gap < slack_s_ ? std::max(0.0, gap) : 0.75 * slack_s_ + 0.25 * gap;
+    // time from the previous D2H's end to this issue: what deferred host
+    // hashing can use
+    const double gap2 = prev_landed < 0 ? 0.0 : static_cast<double>(t0 - prev_landed) / 1e9;
+    slack_d2h_s_ = gap2 > 120 ? 0 : gap2 < slack_d2h_s_ ? std::max(0.0, gap2) : 0.75 * slack_d2h_s_ + 0.25 * gap2;
   }
   if (hash_bytes_.load() > (256ull << 20)) {  // host hashing rate of the previous jobs
     const double per_thread = static_cast<double>(hash_bytes_.load()) / std::max<double>(1, hash_busy_ns_.load()) * 1e9;
@@ -519,6 +533,9 @@ std::shared_ptr<ticket_state> engine::issue(const std::shared_ptr<session>& sp, 
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
 
   auto j = std::make_shared<job>();
+  j->slack_s = slack_s_;
+  j->slack_d2h_s = slack_d2h_s_;
+  j->host_rate = host_rate_;
   j->sess = sp;
   j->rank_id = rank.rank_id;
   j->iteration = iteration;
@@ -691,20 +708,32 @@ void engine::prepare(const std::shared_ptr<job>& j, const ts_rank_info& rank, co
       // the GPU; host workers are worth it only for the slack before the next
       // checkpoint (a training loop). A closed loop (caller waits for persist,
       // no slack) keeps everything on the GPU, so host-held pool windows can
-      // never throttle the D2H. One host chain must finish within D2H + slack.
-      const double d2h_s = static_cast<double>(j->img) / 50e9;
-      // (experiment knob TS_HOST_CK_D2H=1: the host may also use the D2H time
-      // itself when there is slack, i.e. a training loop)
-      static const bool with_d2h = std::getenv("TS_HOST_CK_D2H") != nullptr;
-      const double budget = slack_s_ + (with_d2h && slack_s_ > 0 ? d2h_s : 0.0);
-      frac = dev_bytes ? std::min(1.0, 0.8 * host_rate_ * budget / static_cast<double>(dev_bytes)) : 0.0;
-      obj_cap = 0.8 * chain_rate_ * (d2h_s + slack_s_);
+      // never throttle the D2H.
+      //
       // Host-hashed windows that land in the pinned pool hold it until hashed:
       // only when the pool takes all of them can hashing not throttle the D2H.
       uint64_t pool_bytes = 0;
       for (const auto& f : j->files)
         if (!(j->io && f.dma)) pool_bytes += f.tre - header_reserved;
+      // Optional (TS_HOST_CK_DEFER=1): when every window lands in a
+      // page-locked file (rotation), the host hashes after the D2H: its budget
+      // is the time from the end of the D2H to the next issue and every host
+      // object is complete from the start (4 chains per worker). Measured on
+      // cfg4 it takes ~47 % of the bytes and cuts the GPU-side cost from
+      // +4.0 % to +3.2 %, but the step slows more overall (5.3-5.6 % vs
+      // 4.1-4.9 %: 16 workers hashing flat out right after the D2H also slow
+      // the training process's host side), so hashing as windows land stays
+      // the default (profiles/r2_defer_ab.jsonl).
+      const char* dv = std::getenv("TS_HOST_CK_DEFER");
+      const bool want_defer = dv && dv[0] == '1';
+      const double d2h_s = static_cast<double>(j->img) / 50e9;
+      const bool defer = want_defer && pool_bytes == 0 && j->io && j->slack_s > 0.05;
+      const double budget = defer ? j->slack_d2h_s : j->slack_s;
+      frac = dev_bytes ? std::min(1.0, 0.8 * j->host_rate * budget / static_cast<double>(dev_bytes)) : 0.0;
+      // one host chain must finish within the budget
+      obj_cap = 0.8 * chain_rate_ * (defer ? j->slack_d2h_s : d2h_s + j->slack_s);
       if (pool_bytes > pool_->capacity()) frac = 0.0;
+      j->defer_hash = defer && frac > 0;
     }
     uint64_t seen = 0, host = 0;
     for (size_t k = 0; k < j->raws.size(); ++k) {
@@ -1158,6 +1187,13 @@ void engine::run_job(const std::shared_ptr<job>& j) {
         cuda_check(cudaStreamWaitEvent(pack_stream_, j->chunk_events[c - nslots], 0), "slot wait");
         if (nf) cuda_check(cudaStreamWaitEvent(pack_stream_, j->ck_events[c - nslots], 0), "slot wait");
       }
+      // Packs and the previous chunk's pack-priority checksums take turns on
+      // the SMs instead of splitting them (same total work; a pack that
+      // shares the GPU with FNV kernels runs at 0.80 instead of 0.91 of the
+      // HBM roofline). Low-priority checksums (the last ring-full) are never
+      // waited for here: they must not delay the capture.
+      if (nf && c > 0 && c - 1 + nslots < nchunks && j->ck_events[c - 1])
+        cuda_check(cudaStreamWaitEvent(pack_stream_, j->ck_events[c - 1], 0), "pack after checksums");
       cudaEvent_t pa, pb;
       cuda_check(cudaEventCreate(&pa), "event");
       cuda_check(cudaEventCreate(&pb), "event");
@@ -1436,13 +1472,18 @@ void engine::window_landed(const std::shared_ptr<job>& j, size_t wi) {
   {
     std::lock_guard<std::mutex> g(j->mu);
     last = j->wins_landed == j->wins.size();
+    if (last) j->t_landed_all = now_ns();
   }
   if (last)
     for (size_t f = 0; f < j->files.size(); ++f) file_progress(j, f);
   else if (j->io && w.dma)
     for (uint32_t k = w.fs_begin; k < w.fs_end; ++k) file_progress(j, j->fs[k].f);
-  for (size_t k = 0; k < (newly_ready + 3) / 4; ++k)
-    workers_->submit(guarded(j, [this, j] { hash_task(j, 0); }));
+  if (!j->defer_hash) {
+    for (size_t k = 0; k < (newly_ready + 3) / 4; ++k)
+      workers_->submit(guarded(j, [this, j] { hash_task(j, 0); }));
+  } else if (last) {  // deferred: every worker drains the ready objects, 4 chains each
+    for (int k = 0; k < workers_->size(); ++k) workers_->submit(guarded(j, [this, j] { hash_task(j, 0); }));
+  }
   if (j->io && !w.dma && w.fs_end > w.fs_begin)
     workers_->submit(guarded(j, [this, j, wi] { flush_window(j, wi); }));
   check_snapshot(j);

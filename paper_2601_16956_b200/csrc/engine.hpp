@@ -215,7 +215,7 @@ class engine {
   std::vector<std::shared_ptr<job>> retired_;  // dropped by the copier (under mu_)
   std::string spare_dir_;  // recycled files of retired checkpoints (retire_checkpoint)
   // checksum placement (auto): host hashing capacity, measured per job
-  double host_rate_ = 0, chain_rate_ = 0.45e9, slack_s_ = 0;
+  double host_rate_ = 0, chain_rate_ = 0.45e9, slack_s_ = 0, slack_d2h_s_ = 0;
   std::atomic<uint64_t> hash_bytes_{0}, hash_busy_ns_{0};
   std::thread copier_, completer_;
 };

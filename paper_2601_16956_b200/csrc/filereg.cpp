@@ -1,5 +1,6 @@
 // Registry of page-locked checkpoint-file mappings (see filereg.hpp).
 #include "filereg.hpp"
+#include "core.hpp"
 
 #include <cuda_runtime.h>
 #include <fcntl.h>
@@ -70,9 +71,12 @@ file_registry& file_registry::get() {
 void file_registry::drop_locked(std::map<file_key, entry>::iterator it) {
   entry& e = it->second;
   if (e.map) {
+    const int64_t t0 = now_ns();
     cudaHostUnregister(e.map);
     cudaGetLastError();
     ::munmap(e.map, e.maplen);
+    stats_[3] += 1;
+    stats_[4] += static_cast<uint64_t>(now_ns() - t0);
   }
   if (e.fd >= 0) ::close(e.fd);
   m_.erase(it);
@@ -204,7 +208,14 @@ void file_registry::register_file(const file_key& key, int device) {
   void* m = ok ? ::mmap(nullptr, ml, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0) : MAP_FAILED;
   ok = m != MAP_FAILED;
   bool refused = false;
-  if (ok && cudaHostRegister(m, ml, cudaHostRegisterPortable | cudaHostRegisterMapped) != cudaSuccess) {
+  const int64_t t_reg = now_ns();
+  const bool reg_ok = ok && cudaHostRegister(m, ml, cudaHostRegisterPortable | cudaHostRegisterMapped) == cudaSuccess;
+  if (ok) {
+    stats_[0] += 1;
+    stats_[1] += static_cast<uint64_t>(now_ns() - t_reg);
+    if (reg_ok) stats_[2] += ml;
+  }
+  if (ok && !reg_ok) {
     cudaGetLastError();
     ::munmap(m, ml);
     ok = false;
@@ -263,4 +274,10 @@ uint64_t file_registry::registered_bytes() {
   return b;
 }
 
+}  // namespace tsb
+
+namespace tsb {
+void file_registry::stats(uint64_t out[5]) {
+  for (int i = 0; i < 5; ++i) out[i] = stats_[i].load();
+}
 }  // namespace tsb

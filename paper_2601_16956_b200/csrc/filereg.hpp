@@ -26,6 +26,7 @@
 
 #include <condition_variable>
 #include <cstdint>
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <set>
@@ -69,6 +70,9 @@ class file_registry {
   // Drop every idle registration; returns bytes released.
   uint64_t release_all();
   uint64_t registered_bytes();
+  // [registrations, ns inside cudaHostRegister, bytes registered,
+  //  unregistrations, ns inside cudaHostUnregister + munmap] since start
+  void stats(uint64_t out[5]);
 
  private:
   struct entry {
@@ -80,6 +84,7 @@ class file_registry {
     int64_t size = -1, mtime_ns = -1;
   };
   void drop_locked(std::map<file_key, entry>::iterator it);
+  std::atomic<uint64_t> stats_[5] = {{0}, {0}, {0}, {0}, {0}};
   std::mutex mu_;
   std::map<file_key, entry> m_;
   std::set<uint64_t> unsupported_dev_;  // filesystems whose pages cannot be locked

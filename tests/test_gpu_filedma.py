@@ -293,3 +293,58 @@ def test_spares_accumulate_up_to_limit(gpu, shm):
     for n in names:
         per.setdefault(n.split(".bin")[0], []).append(n)
     assert per and all(1 <= len(v) <= 4 for v in per.values())
+
+
+@pytest.mark.parametrize("defer", ["0", "1"])
+def test_auto_host_hashing_in_a_training_loop(gpu, defer, monkeypatch):
+    """Auto checksum placement in a lazy loop with slack between checkpoints
+    and rotation on tmpfs (every window lands in a page-locked file): the host
+    workers take a share — as windows land, or after the D2H with
+    TS_HOST_CK_DEFER=1. Every checkpoint's footers verify and the last one
+    restores bit-exactly."""
+    if not os.path.isdir("/dev/shm"):
+        pytest.skip("needs tmpfs for page-locked files")
+    monkeypatch.setenv("TS_HOST_CK_DEFER", defer)
+    tmp = tempfile.mkdtemp(dir="/dev/shm")
+    try:
+        _auto_host_hashing_loop(tmp)
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+        api.file_cache_release_all()
+
+
+def _auto_host_hashing_loop(tmp):
+    import time
+
+    spec = S.RankSpec(0, seed=11, metadata_bytes=256)
+    for i in range(24):
+        spec.objects.append(S.ObjSpec(i + 1, 0, 0, 1, i % 3, (5 << 20) + 4096 * i + 13, S.pack_space(2, i, 0), 0))
+    spec.objects.append(S.ObjSpec(100, 1, 1, 2, 0, meta=("meta",)))
+    st = api.materialize_payloads(spec, 0, 1)
+    spare = os.path.join(tmp, ".spare")
+    eng = api.CheckpointEngine(api.EngineConfig(raw_chunk_bytes=4 << 20, staging_capacity_bytes=64 << 20,
+                                                device_staging_bytes=32 << 20, flush_workers=4), 0, 0)
+    eng.set_spare_dir(spare)
+    prev, host_bytes = None, []
+    for it in range(1, 9):
+        api.mutate_update_step(st, it)
+        d = os.path.join(tmp, f"c{it}")
+        sess = api.CheckpointSession(d, it, it, None, 1)
+        t = eng.issue_checkpoint(sess, st, it)
+        eng.pre_update_barrier(t, host_block=1)
+        t.wait_persisted()
+        sess.wait_complete(60)
+        host_bytes.append(t.stats()["host_checksum_bytes"])
+        assert api.verify_checkpoint(os.path.join(d, "MANIFEST.tlv")).ok
+        if prev:
+            api.retire_checkpoint(prev, spare)
+        prev = d
+        time.sleep(0.4)  # slack: the training step between checkpoints
+    eng.shutdown()
+    assert max(host_bytes[3:]) > 0, host_bytes  # the auto policy handed the host a share
+    rs = api.restore_checkpoint(os.path.join(prev, "MANIFEST.tlv"))[0]
+    for o, so in zip(rs.objects, spec.objects):
+        o.pattern_space, o.pattern_offset = so.space, so.offset
+    rs.seed = spec.seed
+    assert api.pattern_mismatches(api.RankState(0, seed=spec.seed, objects=[o for o in rs.objects if o.is_raw()]),
+                                  8) == 0
