@@ -864,6 +864,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0, snap_ms):
                              for m, v in phases.items() if v},
             "fwd_bwd_gpu_ms_max": {m: round(max(v), 1) for m, v in fb_gpu.items() if v},
             "page_lock_in_blocks": {m: {k: round(v, 1) for k, v in d.items()} for m, d in page_lock.items()},
+            "fwd_bwd_event_record_ms_per_step": {m: [round(1e3 * x[1], 2) for x in v] for m, v in phases.items() if v},
             "clocks": {m: {"sm_mhz": [c["sm_mhz"] for c in v], "power_w": [c.get("power_w") for c in v],
                            "reasons": sorted({r for c in v for r in c["reasons"]})} for m, v in clk.items()},
             "checkpoints_to": (f"files on /dev/shm, rotation keeps {args.keep}, file_dma bytes of the last "
