@@ -313,8 +313,13 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
   // a stream callback frees the slot. Reads run up to K windows ahead.
   // (large windows: fewer, longer unpack launches — 1 GiB: 90 % of the HBM
   // roofline vs 82-85 % at 256 MiB; small restores keep small staging)
-  const int K = 4;
+  // Tuning knobs for experiments (defaults measured best, profiles/r2_restore_knobs.log):
+  // TS_RESTORE_WINDOWS (ring depth), TS_RESTORE_READ_MB (pread piece).
+  const char* kw = std::getenv("TS_RESTORE_WINDOWS");
+  const int K = std::max(2, std::min(8, kw ? std::atoi(kw) : 4));  // (slot_busy holds 8)
   const uint64_t W = std::min<uint64_t>(1ull << 30, std::max<uint64_t>(64ull << 20, align_up(img / K + 1, 2ull << 20)));
+  const char* rp = std::getenv("TS_RESTORE_READ_MB");
+  const uint64_t read_piece = static_cast<uint64_t>(std::max(1, std::min(1024, rp ? std::atoi(rp) : 16))) << 20;
   // One restore at a time uses the rings: take the lock first and size them
   // under it, so a concurrent restore cannot reallocate them in between.
   std::lock_guard<std::mutex> stage_guard(g_stage_mu);
@@ -549,7 +554,7 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
           direct = true;  // no pread: the copy engine reads the locked pages
           continue;
         }
-        for (uint64_t x = a; x < b; x += (16ull << 20)) reads.emplace_back(k, x, std::min<uint64_t>(b, x + (16ull << 20)));
+        for (uint64_t x = a; x < b; x += read_piece) reads.emplace_back(k, x, std::min<uint64_t>(b, x + read_piece));
       }
       if (reads.empty()) {
         try {
