@@ -409,6 +409,7 @@ def ours(args):
                            checksum_priority=args.ck_priority, pack_priority=args.pack_priority,
                            checksum_host_frac=args.ck_host_frac, ring_chunk_bytes=int(args.ring_chunk_gb * (1 << 30)),
                            worker_nice=args.worker_nice, helper_devices=helpers, helper_share=share,
+                           checksum_lane_max_bytes=-1 if args.lane_max_mb < 0 else int(args.lane_max_mb * (1 << 20)),
                            flush_mmap=3 if args.flush_uring else 2 if args.flush_direct else int(not args.flush_pwrite))
     eng = api.CheckpointEngine(cfg, spec.rank_id, local_dev)
     numa_node = eng.numa_node
@@ -655,6 +656,11 @@ def ours(args):
                        "checksums": "host" if args.host_checksum else "gpu", "pack_kernel": args.pack_kernel,
                        "priorities": {"pack": args.pack_priority, "checksums": args.ck_priority},
                        "checksum_host_frac": "auto" if args.ck_host_frac < 0 else args.ck_host_frac,
+                       "checksum_lane_max": ("auto" if args.lane_max_mb < 0 else
+                                             f"{args.lane_max_mb} MiB" if args.lane_max_mb > 0 else "off"),
+                       "lane_checksum_frac": round(statistics.mean(s["lane_checksum_bytes"] for s in stats)
+                                                   / max(1, bytes_step), 3),
+                       "lane_ms": round(statistics.mean(s["lane_ms"] for s in stats), 1),
                        "numa_node": numa_node, "shared_gpu": share_gpu,
                        "d2h_helpers": {"devices": list(helpers), "share": round(share, 3)},
                        "step": "update(pattern kernel) + issue + snapshot + checksums (no files)"},
@@ -733,7 +739,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0, snap_ms):
     ckpts = []  # (dir, session, ticket) on disk, oldest first
     comp = torch.cuda.current_stream()
     res = {"off": ([], []), "lazy": ([], [])}
-    host_ck, ck_tickets = [], []
+    host_ck, lane_ck, ck_tickets = [], [], []
     page_lock = {}  # file-registry page-lock activity inside the timed blocks (holds the driver)
     issue_cpp, issue_py = [], []  # issue time inside the engine vs the whole Python call
     clk = {"off": [], "lazy": []}
@@ -832,6 +838,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0, snap_ms):
         for tk in ck_tickets:
             tk.wait_persisted()
             host_ck.append(tk.stats()["host_checksum_bytes"] / max(1, spec.raw_bytes))
+            lane_ck.append(tk.stats()["lane_checksum_bytes"] / max(1, spec.raw_bytes))
         ck_tickets.clear()
     res = {m: (statistics.mean(t), statistics.mean(b) if b else 0.0) for m, (t, b) in res.items()}
     eng.shutdown()
@@ -850,6 +857,7 @@ def training_phase(args, api, state, spec, cfg, local, dev, it0, snap_ms):
             "slowdown_pct": round(100 * (lazy - off) / off, 2),
             "blocked_ms_per_ckpt": round(res["lazy"][1], 3),
             "host_checksum_frac": round(statistics.mean(host_ck), 3) if host_ck else None,
+            "lane_checksum_frac": round(statistics.mean(lane_ck), 3) if lane_ck else None,
             "rotation_wait_ms": round(1e3 * statistics.mean(rot_wait), 2) if rot_wait else None,
             "issue_ms": {"engine": round(statistics.mean(issue_cpp), 3) if issue_cpp else None,
                          "python_call": round(statistics.mean(issue_py), 3) if issue_py else None},
@@ -900,6 +908,8 @@ def main():
     ap.add_argument("--ck-host-frac", type=float, default=-1.0,
                     help="share of checksums on host workers (0: all GPU; <0: auto from host rate and cadence)")
     ap.add_argument("--pack-priority", type=int, default=1, help="capture (pack) stream priority (1/0/-1)")
+    ap.add_argument("--lane-max-mb", type=float, default=0.0,
+                    help="lane-serial device checksums for objects up to this size (0 off, -1 auto)")
     ap.add_argument("--flush-workers", type=int, default=0, help="host worker threads (default: min(16, cores))")
     ap.add_argument("--keep", type=int, default=1, help="e2e rotation: checkpoints kept on tmpfs")
     ap.add_argument("--ckpt-root", default="", help="e2e checkpoint directory root (default /dev/shm)")

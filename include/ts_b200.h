@@ -212,6 +212,12 @@ typedef struct ts_engine_config {
                                        (cfg2's dp-0 rank). 0 (default): none */
   uint32_t _pad4;
   double helper_share;              /* fraction of the image the helpers carry, spread evenly */
+  int64_t checksum_lane_max_bytes;  /* RING device checksums: objects up to this size are hashed by
+                                       the lane-serial FNV kernel (one lane per object, ~7 integer
+                                       ops per byte instead of ~26) straight from the state, before
+                                       the capture completes. 0 (default): off (segment-parallel
+                                       kernels only); -1: auto — in a multi-slot ring, objects a
+                                       lane (~85 MB/s) finishes within 40 % of the capture time */
 } ts_engine_config;
 
 void ts_engine_config_default(ts_engine_config* cfg);
@@ -307,6 +313,9 @@ typedef struct ts_ticket_stats {
   uint64_t host_checksum_bytes; /* device-tier bytes hashed by host workers (rest: FNV kernels) */
   uint64_t helper_bytes;        /* image bytes D2H'd by helper GPUs (helper_mask) */
   uint64_t direct_io_bytes;     /* fixed-region bytes written with O_DIRECT (flush_mmap = 2) */
+  uint64_t lane_checksum_bytes; /* device-tier bytes hashed by the lane-serial FNV kernel */
+  float lane_ms;                /* CUDA-event time of the lane-serial FNV kernel */
+  uint32_t _pad5;
 } ts_ticket_stats;
 ts_status ts_ticket_stats_get(ts_ticket* t, ts_ticket_stats* out);
 /* Per-object checksum accumulated at staging (transfer.cpp:163-166) */
@@ -408,6 +417,10 @@ ts_status ts_pattern_verify(const ts_pattern_desc* d, size_t n, uint64_t seed,
  * results land in host `out`. Synchronous w.r.t. the host. */
 ts_status ts_fnv1a64_device(const void* const* ptrs, const uint64_t* sizes, size_t n,
                             const uint64_t* init, uint64_t* out, void* stream);
+/* Same result, lane-serial kernel (one lane per range, ~7 integer ops per byte;
+ * a range's time is its length at ~0.2 GB/s). B200-side addition. */
+ts_status ts_fnv1a64_device_lanes(const void* const* ptrs, const uint64_t* sizes, size_t n,
+                                  const uint64_t* init, uint64_t* out, void* stream);
 
 /* Raw kernel entry for microbenchmarks: gather `n` device fragments into `dst`
  * (device or mapped-host) at dst_offsets, zero-filling the gaps up to `dst_len`. */

@@ -104,7 +104,8 @@ class EngineConfigC(C.Structure):
                 ("bulk_min_bytes", C.c_uint64), ("file_dma", C.c_int32), ("checksum_priority", C.c_int32),
                 ("_pad2", C.c_int32), ("checksum_host_frac", C.c_double), ("ring_chunk_bytes", C.c_uint64),
                 ("numa_bind", C.c_int32), ("worker_nice", C.c_int32),
-                ("helper_mask", C.c_uint32), ("_pad4", C.c_uint32), ("helper_share", C.c_double)]
+                ("helper_mask", C.c_uint32), ("_pad4", C.c_uint32), ("helper_share", C.c_double),
+                ("checksum_lane_max_bytes", C.c_int64)]
 
 
 class ManifestEcho(C.Structure):
@@ -122,7 +123,8 @@ class TicketStats(C.Structure):
                 ("copies", C.c_uint32), ("snapshot_done", C.c_int32), ("persisted_done", C.c_int32),
                 ("failed", C.c_int32), ("file_dma_bytes", C.c_uint64),
                 ("host_checksum_bytes", C.c_uint64), ("helper_bytes", C.c_uint64),
-                ("direct_io_bytes", C.c_uint64)]
+                ("direct_io_bytes", C.c_uint64), ("lane_checksum_bytes", C.c_uint64), ("lane_ms", C.c_float),
+                ("_pad5", C.c_uint32)]
 
 
 class RestoreObject(C.Structure):
@@ -234,6 +236,7 @@ _sig("ts_pack", i32, C.POINTER(P), C.POINTER(u64), C.POINTER(u64), sz, P, u64, i
 _sig("ts_unpack", i32, P, C.POINTER(u64), C.POINTER(P), C.POINTER(u64), sz, i32, i32, P)
 _sig("ts_kernel_launch_count", u64)
 _sig("ts_fnv1a64_device", i32, C.POINTER(P), C.POINTER(u64), sz, C.POINTER(u64), C.POINTER(u64), P)
+_sig("ts_fnv1a64_device_lanes", i32, C.POINTER(P), C.POINTER(u64), sz, C.POINTER(u64), C.POINTER(u64), P)
 
 def call(fn, *args):
     raise_for(fn(*args))

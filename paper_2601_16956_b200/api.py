@@ -233,15 +233,17 @@ def tlv_decode(b: bytes) -> Any:
     return Value.decode(b).to_py()
 
 
-def fnv1a64_device(tensors, init=None, stream=None):
-    """FNV-1a-64 of each device tensor's bytes, computed by the GPU kernels."""
+def fnv1a64_device(tensors, init=None, stream=None, lanes=False):
+    """FNV-1a-64 of each device tensor's bytes, computed by the GPU kernels
+    (segment-parallel; lanes=True: the lane-serial kernel)."""
     n = len(tensors)
     ptrs = (C.c_void_p * max(1, n))(*[t.data_ptr() for t in tensors])
     sizes = (C.c_uint64 * max(1, n))(*[t.numel() * t.element_size() for t in tensors])
     out = (C.c_uint64 * max(1, n))()
     ini = (C.c_uint64 * max(1, n))(*init) if init is not None else None
     sh = _stream_handle(stream)
-    N.call(N.lib.ts_fnv1a64_device, ptrs, sizes, n, ini, out, C.c_void_p(sh))
+    fn = N.lib.ts_fnv1a64_device_lanes if lanes else N.lib.ts_fnv1a64_device
+    N.call(fn, ptrs, sizes, n, ini, out, C.c_void_p(sh))
     return list(out)[:n]
 
 
@@ -355,6 +357,7 @@ class EngineConfig:
     worker_nice: int = 19  # nice increment of the background worker threads (0 = none)
     helper_devices: tuple = ()  # RING: GPUs whose copy engines carry part of this rank's D2H (NVLink read)
     helper_share: float = 0.0  # fraction of the image they carry
+    checksum_lane_max_bytes: int = 0  # lane-serial FNV for objects up to this size (0 off, -1 auto)
 
     def to_c(self) -> N.EngineConfigC:
         c = N.EngineConfigC()
@@ -387,6 +390,7 @@ class EngineConfig:
         c.worker_nice = int(self.worker_nice)
         c.helper_mask = sum(1 << int(d) for d in self.helper_devices)
         c.helper_share = float(self.helper_share)
+        c.checksum_lane_max_bytes = int(self.checksum_lane_max_bytes)
         return c
 
 

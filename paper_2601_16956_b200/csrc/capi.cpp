@@ -2,6 +2,7 @@
 // entry point maps tsb::error to its ts_status and records the message.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <memory>
 
 #include "engine.hpp"
@@ -206,6 +207,7 @@ void ts_engine_config_default(ts_engine_config* c) {
   c->worker_nice = 19;
   c->helper_mask = 0;
   c->helper_share = 0.0;
+  c->checksum_lane_max_bytes = 0;
 }
 
 ts_status ts_engine_create(const ts_engine_config* cfg, int rank_id, int device, ts_engine** out) {
@@ -373,6 +375,8 @@ ts_status ts_ticket_stats_get(ts_ticket* t, ts_ticket_stats* o) {
     o->host_checksum_bytes = s.host_checksum_bytes;
     o->helper_bytes = s.helper_bytes;
     o->direct_io_bytes = s.direct_io_bytes;
+    o->lane_checksum_bytes = s.lane_checksum_bytes;
+    o->lane_ms = s.lane_ms;
   });
 }
 
@@ -647,6 +651,30 @@ ts_status ts_fnv1a64_device(const void* const* ptrs, const uint64_t* sizes, size
     dev::launch_fnv(reinterpret_cast<dev::fnv_obj*>(buf), static_cast<uint32_t>(n), nseg, nchunk,
                     reinterpret_cast<uint64_t*>(buf + tb), buf + tb + sb, st);
     cuda_check(cudaGetLastError(), "fnv launch");
+    cuda_check(cudaMemcpyAsync(out, buf + tb, n * 8, cudaMemcpyDeviceToHost, st), "download");
+    cuda_check(cudaFreeAsync(buf, st), "free");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+ts_status ts_fnv1a64_device_lanes(const void* const* ptrs, const uint64_t* sizes, size_t n, const uint64_t* init,
+                                  uint64_t* out, void* stream) {
+  return guard([&] {
+    require_device();
+    if (n == 0) return;
+    auto st = static_cast<cudaStream_t>(stream);
+    std::vector<dev::fnv_lane_obj> objs(n);
+    for (size_t i = 0; i < n; ++i)
+      objs[i] = {static_cast<const uint8_t*>(ptrs[i]), sizes[i], init ? init[i] : fnv_seed, i};
+    std::stable_sort(objs.begin(), objs.end(), [](const auto& a, const auto& b) { return a.len > b.len; });
+    const uint64_t tb = dev::align_up_dev(n * sizeof(dev::fnv_lane_obj), 256);
+    uint8_t* buf = nullptr;
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&buf), tb + n * 8, st), "alloc");
+    cuda_check(cudaMemcpyAsync(buf, objs.data(), n * sizeof(dev::fnv_lane_obj), cudaMemcpyHostToDevice, st),
+               "upload");
+    dev::launch_fnv_lanes(reinterpret_cast<dev::fnv_lane_obj*>(buf), static_cast<uint32_t>(n),
+                          reinterpret_cast<uint64_t*>(buf + tb), st);
+    cuda_check(cudaGetLastError(), "fnv lane launch");
     cuda_check(cudaMemcpyAsync(out, buf + tb, n * 8, cudaMemcpyDeviceToHost, st), "download");
     cuda_check(cudaFreeAsync(buf, st), "free");
     cuda_check(cudaStreamSynchronize(st), "sync");

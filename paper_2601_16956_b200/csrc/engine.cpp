@@ -44,6 +44,11 @@ void mkdirs(const std::string& path) {
 
 namespace {
 const bool g_trace = std::getenv("TS_TRACE") != nullptr;
+// Per-lane rate of the lane-serial FNV kernel, measured on B200 (alone and
+// beside the training load alike: 131 MB in 1.52-1.54 s,
+// profiles/r2_lanes_kernel.jsonl): sizes the auto object cap
+// (checksum_lane_max_bytes < 0).
+constexpr double kLaneBytesPerS = 0.085e9;
 const bool g_trace_copies = std::getenv("TS_TRACE_COPIES") != nullptr;  // per-job enqueue cost summary
 #define TRACE(...)                                                                     \
   do {                                                                                 \
@@ -189,6 +194,9 @@ struct job {
   std::vector<uint32_t> fnv_objs;
   uint64_t* fnv_out = nullptr;  // engine's mapped results buffer
   cudaEvent_t fnv_ev = nullptr;
+  // lane-serial checksums (RING): launched at the start of the capture over the
+  // state; the capture and the results' publication wait for lane_ev1
+  cudaEvent_t lane_ev0 = nullptr, lane_ev1 = nullptr;
 
   ~job() {
     for (auto& f : files)  // a claimed file that never finalized: its pages may be stale
@@ -201,6 +209,8 @@ struct job {
       cudaEventDestroy(pe.first);
       cudaEventDestroy(pe.second);
     }
+    if (lane_ev0) cudaEventDestroy(lane_ev0);
+    if (lane_ev1) cudaEventDestroy(lane_ev1);
   }
 
   std::mutex mu;
@@ -266,6 +276,17 @@ engine::engine(const ts_engine_config& cfg, int rank_id, int device)
   // after its checksums, so those run at the pack's priority (at low priority
   // they starve behind back-to-back training kernels and stall the capture)
   cuda_check(cudaStreamCreateWithPriority(&ck_hi_stream_, cudaStreamNonBlocking, pack_prio), "stream");
+  // Lane-serial checksums read the state, so the capture waits for them: a
+  // few warps for most of the D2H, at the pack's priority (TS_LANE_PRIO
+  // overrides: 1 / 0 / -1, for A/B runs).
+  {
+    int lp = pack_prio;
+    if (const char* e = std::getenv("TS_LANE_PRIO")) {
+      const int v = std::atoi(e);
+      lp = v > 0 ? hi_prio : v < 0 ? lo_prio : 0;
+    }
+    cuda_check(cudaStreamCreateWithPriority(&ck_lane_stream_, cudaStreamNonBlocking, lp), "stream");
+  }
   // Workers (checksums, flushes, serialization, page locking) are background
   // work: a lower CPU priority keeps the training process's kernel-launching
   // thread responsive when every core is hashing.
@@ -312,6 +333,7 @@ engine::~engine() {
   if (pack_stream_) cudaStreamDestroy(pack_stream_);
   if (ck_stream_) cudaStreamDestroy(ck_stream_);
   if (ck_hi_stream_) cudaStreamDestroy(ck_hi_stream_);
+  if (ck_lane_stream_) cudaStreamDestroy(ck_lane_stream_);
   for (auto& h : helpers_) {
     cudaSetDevice(h->dev);
     for (auto e : h->free_ev) cudaEventDestroy(e);
@@ -907,6 +929,7 @@ void engine::copier_loop() {
     {
       std::lock_guard<std::mutex> g(j->t->mu);
       if (!j->t->capture_recorded) {
+        if (j->lane_ev1) cudaStreamWaitEvent(pack_stream_, j->lane_ev1, 0);
         cudaEventRecord(j->t->ev_capture, pack_stream_);
         j->t->capture_recorded = true;
       }
@@ -1059,10 +1082,41 @@ void engine::run_job(const std::shared_ptr<job>& j) {
   // piece), grouped by chunk; launch k covers entries [cbeg[k], cbeg[k+1]).
   const uint32_t nf = static_cast<uint32_t>(j->fnv_objs.size());
   uint8_t* fbuf = nullptr;
-  uint64_t ftb = 0, fsb = 0;
+  uint64_t ftb = 0, fsb = 0, lane_off = 0;
   std::vector<dev::fnv_obj> fo;
   std::vector<size_t> cbeg;
   std::vector<std::pair<uint64_t, uint64_t>> cdims;  // (nseg, nchunk) per launch
+  // Lane-serial checksums (RING): objects one lane hashes well within the
+  // capture time are hashed from the state itself at ~7 integer ops per byte
+  // (a few warps, most of the D2H long) instead of by the speculating
+  // segment-parallel kernels over the ring slots (~26 ops per byte).
+  std::vector<char> lane_q;
+  std::vector<dev::fnv_lane_obj> lanes;
+  uint64_t lane_bytes = 0;
+  if (nf && use_ring) {
+    uint64_t lane_max = 0;
+    if (cfg_.checksum_lane_max_bytes > 0) {
+      lane_max = static_cast<uint64_t>(cfg_.checksum_lane_max_bytes);
+    } else if (cfg_.checksum_lane_max_bytes < 0 && nslots > 1) {
+      // the capture completes once all but the last ring-full has left the
+      // device over PCIe (>= 50 GB/s): a lane gets 40 % of that time
+      const double cap_s = static_cast<double>(j->img - std::min<uint64_t>(j->img, nslots * chunk)) / 50e9;
+      lane_max = static_cast<uint64_t>(0.4 * kLaneBytesPerS * cap_s);
+    }
+    if (lane_max) {
+      lane_q.assign(nf, 0);
+      for (uint32_t q = 0; q < nf; ++q) {
+        const auto& r = j->raws[j->fnv_objs[q]];
+        if (r.size > lane_max) continue;
+        lane_q[q] = 1;
+        lanes.push_back({r.src, r.size, fnv_seed, q});
+        lane_bytes += r.size;
+      }
+      // longest first: the lanes of a warp finish together
+      std::stable_sort(lanes.begin(), lanes.end(),
+                       [](const dev::fnv_lane_obj& a, const dev::fnv_lane_obj& b) { return a.len > b.len; });
+    }
+  }
   if (nf) {
     if (use_ring) {
       size_t k = 0;  // fnv_objs are in image order
@@ -1071,6 +1125,7 @@ void engine::run_job(const std::shared_ptr<job>& j) {
         const uint64_t clo = c * chunk, chi = std::min(j->img, clo + chunk);
         while (k < nf && j->raws[j->fnv_objs[k]].img + j->raws[j->fnv_objs[k]].size <= clo) ++k;
         for (size_t q = k; q < nf && j->raws[j->fnv_objs[q]].img < chi; ++q) {
+          if (!lane_q.empty() && lane_q[q]) continue;
           const auto& r = j->raws[j->fnv_objs[q]];
           const uint64_t a = std::max(clo, r.img), b = std::min(chi, r.img + r.size);
           fo.push_back({ring + (nslots == 1 ? 0 : (c % nslots) * chunk) + (a - clo), b - a, 0, 0, q});
@@ -1094,12 +1149,18 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     }
     ftb = align_up(fo.size() * sizeof(dev::fnv_obj), 256);
     fsb = align_up(nf * 8ull, 256);
-    fbuf = ensure_fnv_buffer(ftb + fsb + max_scratch);
+    lane_off = ftb + fsb + align_up(max_scratch, 256);
+    fbuf = ensure_fnv_buffer(lane_off + lanes.size() * sizeof(dev::fnv_lane_obj));
     std::vector<uint64_t> seeds(nf, fnv_seed);
-    cuda_check(cudaMemcpyAsync(fbuf, fo.data(), fo.size() * sizeof(dev::fnv_obj), cudaMemcpyHostToDevice,
-                               pack_stream_), "upload checksum table");
+    if (!fo.empty())  // (empty when the lane kernel takes every object)
+      cuda_check(cudaMemcpyAsync(fbuf, fo.data(), fo.size() * sizeof(dev::fnv_obj), cudaMemcpyHostToDevice,
+                                 pack_stream_), "upload checksum table");
     cuda_check(cudaMemcpyAsync(fbuf + ftb, seeds.data(), nf * 8ull, cudaMemcpyHostToDevice, pack_stream_),
                "upload checksum seeds");
+    if (!lanes.empty())
+      cuda_check(cudaMemcpyAsync(fbuf + lane_off, lanes.data(), lanes.size() * sizeof(dev::fnv_lane_obj),
+                                 cudaMemcpyHostToDevice, pack_stream_),
+                 "upload lane checksum table");
     if (ck_host_n_ < nf) {  // the previous job's results were consumed before its snapshot completed
       if (ck_host_) cudaFreeHost(ck_host_);
       ck_host_ = nullptr;
@@ -1137,6 +1198,7 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     }
     if (k + 2 != cbeg.size()) return;
   publish:
+    if (j->lane_ev1) cuda_check(cudaStreamWaitEvent(cs, j->lane_ev1, 0), "wait lane checksums");
     cuda_check(cudaEventRecord(j->fnv_ev, cs), "event");
     // RING: the completer learns about the results only after the last
     // window, so it never blocks on the checksums ahead of windows whose
@@ -1147,6 +1209,24 @@ void engine::run_job(const std::shared_ptr<job>& j) {
   cuda_check(cudaStreamWaitEvent(pack_stream_, t.ev_start, 0), "wait producer");
   cuda_check(cudaStreamWaitEvent(copy_stream_, t.ev_start, 0), "wait producer");
   cuda_check(cudaEventRecord(t.ev_pack0, mode == TS_D2H_DIRECT ? copy_stream_ : pack_stream_), "event");
+  if (!lanes.empty()) {  // tables uploaded and the producer done: start hashing the state
+    cudaEvent_t ready;
+    cuda_check(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventRecord(ready, pack_stream_), "event");
+    cuda_check(cudaStreamWaitEvent(ck_lane_stream_, ready, 0), "lane checksums wait");
+    cudaEventDestroy(ready);
+    cuda_check(cudaEventCreate(&j->lane_ev0), "event");
+    cuda_check(cudaEventCreate(&j->lane_ev1), "event");
+    uint64_t* out = nullptr;
+    cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&out), j->fnv_out, 0), "cudaHostGetDevicePointer");
+    cuda_check(cudaEventRecord(j->lane_ev0, ck_lane_stream_), "event");
+    dev::launch_fnv_lanes(reinterpret_cast<dev::fnv_lane_obj*>(fbuf + lane_off), static_cast<uint32_t>(lanes.size()),
+                          out, ck_lane_stream_);
+    cuda_check(cudaGetLastError(), "lane checksum kernel");
+    cuda_check(cudaEventRecord(j->lane_ev1, ck_lane_stream_), "event");
+    t.kernel_launches += 1;
+    t.lane_checksum_bytes = lane_bytes;
+  }
   if (nf && !use_ring) {
     launch_checksums(0, pack_stream_);
     // DIRECT captures on the copy stream: it must also cover the checksum reads.
@@ -1224,7 +1304,11 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       cuda_check(cudaGetLastError(), "pack kernel launch");
       cuda_check(cudaEventCreateWithFlags(&packed_ev[c], cudaEventDisableTiming), "event");
       cuda_check(cudaEventRecord(packed_ev[c], pack_stream_), "event");
-      if (c + 1 == nchunks) mark_capture(pack_stream_);
+      if (c + 1 == nchunks) {
+        // the lane checksums read the state: the capture covers them
+        if (j->lane_ev1) cuda_check(cudaStreamWaitEvent(pack_stream_, j->lane_ev1, 0), "capture after lanes");
+        mark_capture(pack_stream_);
+      }
       if (nf) {  // reads the slot on the checksum stream, overlapping the D2H
         // chunks whose slot is packed again in this job: capture path, pack
         // priority; the last ring-full: low priority (chained states keep the
@@ -1746,6 +1830,7 @@ void engine::check_snapshot(const std::shared_ptr<job>& j) {
         // (events of an empty image were never recorded; a failed query must
         // not leave a stale per-thread error for a later cudaGetLastError)
         j->t->d2h_ms = j->img > 0 ? elapsed_ms(j->t->ev_d2h_first, j->t->ev_d2h_last) : 0.f;
+        if (j->lane_ev1) j->t->lane_ms = elapsed_ms(j->lane_ev0, j->lane_ev1);
         if (!j->pack_events.empty()) {  // RING: sum of the pack kernels alone
           float sum = 0;
           for (auto& pe : j->pack_events) sum += elapsed_ms(pe.first, pe.second);

@@ -103,7 +103,8 @@ struct ticket_state {
   uint64_t host_checksum_bytes = 0;  // device-tier bytes hashed by host workers (rest: FNV kernels)
   uint64_t helper_bytes = 0;         // image bytes D2H'd by helper GPUs' copy engines (NVLink read)
   uint64_t direct_io_bytes = 0;      // fixed-region bytes written O_DIRECT (flush_mmap = 2)
-  float pack_ms = 0, d2h_ms = 0;
+  float pack_ms = 0, d2h_ms = 0, lane_ms = 0;
+  uint64_t lane_checksum_bytes = 0;  // device-tier bytes hashed by the lane-serial FNV kernel
   uint32_t kernel_launches = 0, copies = 0;
   cudaEvent_t ev_start = nullptr, ev_capture = nullptr, ev_d2h_first = nullptr,
               ev_d2h_last = nullptr, ev_pack0 = nullptr;
@@ -188,7 +189,8 @@ class engine {
   std::unique_ptr<pinned_pool> pool_;
   std::unique_ptr<thread_pool> workers_;
   cudaStream_t pack_stream_ = nullptr, copy_stream_ = nullptr, ck_stream_ = nullptr;
-  cudaStream_t ck_hi_stream_ = nullptr;  // checksums a ring slot's reuse (hence the capture) waits for
+  cudaStream_t ck_hi_stream_ = nullptr;
+  cudaStream_t ck_lane_stream_ = nullptr;  // lane-serial checksums over the state (capture path)  // checksums a ring slot's reuse (hence the capture) waits for
   uint8_t* ring_ = nullptr;
   uint64_t ring_bytes_ = 0;
   void* segbuf_ = nullptr;

@@ -212,6 +212,108 @@ __global__ void __launch_bounds__(256) fnv_pass_c(const fnv_obj* __restrict__ o,
 }
 
 // ---------------------------------------------------------------------------
+// Lane-serial FNV: one lane walks one object's whole chain, pass C's split
+// arithmetic started from the object's known state (l = its low byte, c = the
+// upper 56 bits; Horner needs no P^k fix-up then). ~7 integer ops per byte and
+// a critical path of two dependent ops per byte (the low-byte automaton), so a
+// lane runs ~0.2 GB/s and the whole kernel uses a few warps per SM: a tenth of
+// the issue slots the speculating passes take for the same bytes.
+//
+// A lane's loads are its own contiguous stream, so latency is hidden by the
+// lane itself: four 64-B stages in registers, the load of stage k+4 issued as
+// soon as stage k is consumed (~1,500 cycles of work ahead of each load).
+__device__ __forceinline__ uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t c) {
+  uint64_t d;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+}
+
+__global__ void __launch_bounds__(32) fnv_lane_kernel(const fnv_lane_obj* __restrict__ o, uint32_t n,
+                                                      uint64_t* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint8_t* p = o[i].ptr;
+  const uint64_t len = o[i].len;
+  const uint64_t h0 = o[i].init;
+  constexpr uint32_t q = 0x1b3u;
+  constexpr uint64_t kP2 = kP * kP;
+  constexpr uint32_t kP2lo = static_cast<uint32_t>(kP2), kP2hi = static_cast<uint32_t>(kP2 >> 32);
+  uint32_t l = static_cast<uint32_t>(h0) & 0xffu;
+  // c in two 32-bit halves: c * P^2 + e is one wide multiply-add plus two
+  // 32-bit ones (the compiler's 64-bit form spends six instructions)
+  uint32_t clo = static_cast<uint32_t>(h0 >> 8), chi = static_cast<uint32_t>(h0 >> 40);
+  auto step1 = [&](uint32_t b) {
+    const uint32_t x = (l ^ b) & 0xffu;
+    const uint32_t t = x * q;
+    l = t & 0xffu;
+    const uint64_t c = ((static_cast<uint64_t>(chi) << 32) | clo) * kP + ((static_cast<uint64_t>(x) << 32) | (t >> 8));
+    clo = static_cast<uint32_t>(c);
+    chi = static_cast<uint32_t>(c >> 32);
+  };
+  auto step2 = [&](uint32_t b0, uint32_t b1) {
+    const uint32_t x0 = (l ^ b0) & 0xffu;
+    const uint32_t t0 = x0 * q;
+    const uint32_t x1 = (t0 ^ b1) & 0xffu;
+    const uint32_t t1 = x1 * q;
+    l = t1 & 0xffu;
+    const uint32_t d0 = t0 >> 8, d1 = t1 >> 8;
+    const uint32_t e_lo = d0 * q + d1;
+    const uint32_t e_hi = t0 + ((d0 << 8) + x1);
+    const uint64_t w = mad_wide(clo, kP2lo, (static_cast<uint64_t>(e_hi) << 32) | e_lo);
+    const uint32_t hi = clo * kP2hi + (chi * kP2lo + static_cast<uint32_t>(w >> 32));
+    clo = static_cast<uint32_t>(w);
+    chi = hi;
+  };
+  auto word = [&](uint32_t w) {
+    step2(w, w >> 8);
+    step2(w >> 16, w >> 24);
+  };
+  auto vec = [&](const uint4& w) {
+    word(w.x);
+    word(w.y);
+    word(w.z);
+    word(w.w);
+  };
+  const uint64_t head = umin64(len, (16 - (reinterpret_cast<uintptr_t>(p) & 15)) & 15);
+  for (uint64_t k = 0; k < head; ++k) step1(__ldg(p + k));
+  const uint4* v = reinterpret_cast<const uint4*>(p + head);
+  const uint64_t nv = (len - head) >> 4;
+  const uint64_t nb = nv >> 2;  // 64-B blocks
+  uint4 s0[4], s1[4], s2[4], s3[4];
+  auto load = [&](uint4(&s)[4], uint64_t b) {
+    if (b < nb) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s[k] = __ldg(v + 4 * b + k);
+    }
+  };
+  auto proc = [&](const uint4(&s)[4]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) vec(s[k]);
+  };
+  load(s0, 0);
+  load(s1, 1);
+  load(s2, 2);
+  load(s3, 3);
+  uint64_t b = 0;
+  for (; b + 4 <= nb; b += 4) {
+    proc(s0);
+    load(s0, b + 4);
+    proc(s1);
+    load(s1, b + 5);
+    proc(s2);
+    load(s2, b + 6);
+    proc(s3);
+    load(s3, b + 7);
+  }
+  if (b < nb) proc(s0);
+  if (b + 1 < nb) proc(s1);
+  if (b + 2 < nb) proc(s2);
+  for (uint64_t k = nb * 4; k < nv; ++k) vec(__ldg(v + k));
+  for (uint64_t k = head + nv * 16; k < len; ++k) step1(__ldg(p + k));
+  out[o[i].out] = ((((static_cast<uint64_t>(chi) << 32) | clo) & kM56) << 8) | l;
+}
+
+// ---------------------------------------------------------------------------
 // Scans over each object's segments. The per-segment maps (nibble maps for
 // passes A/B, affine maps H -> a*H + c for the combine) compose associatively,
 // so each object's chain is cut into chunks of kChunk segments: compose each
@@ -408,6 +510,13 @@ void launch_fnv(const fnv_obj* d_objs, uint32_t nobj, uint64_t nseg, uint64_t nc
     fnv_chunk_affine<<<gc, T, 0, st>>>(d_objs, nobj, nchunk, pa, ca, cc); L();
   }
   fnv_combine<<<go, T, 0, st>>>(d_objs, nobj, d_states, ca, cc, lo_end, hi_end, out_mapped); L();
+}
+
+void launch_fnv_lanes(const fnv_lane_obj* d_objs, uint32_t n, uint64_t* out, cudaStream_t st) {
+  if (n == 0) return;
+  // one warp per block: the block scheduler spreads the few warps over SMs
+  fnv_lane_kernel<<<(n + 31) / 32, 32, 0, st>>>(d_objs, n, out);
+  count_launch();
 }
 
 }  // namespace tsb::dev

@@ -94,6 +94,20 @@ uint64_t fnv_scratch_bytes(uint64_t nseg, uint64_t nchunk, uint32_t nobj);
 void launch_fnv(const fnv_obj* d_objs, uint32_t nobj, uint64_t nseg, uint64_t nchunk, uint64_t* d_states,
                 void* d_scratch, cudaStream_t st, uint64_t* out_mapped = nullptr);
 
+// Lane-serial FNV-1a-64 (fnv.cu): one lane per object chain, ~7 integer ops per
+// byte (the segment-parallel kernels above spend ~26: nibble speculation).
+// For objects whose serial chain (~0.2 GB/s per lane) finishes within the time
+// budget. Objects should be sorted by length, longest first (lanes of a warp
+// then finish together). Writes out[o.out] = FNV state after o's bytes,
+// starting from o.init.
+struct fnv_lane_obj {
+  const uint8_t* ptr;
+  uint64_t len;
+  uint64_t init;
+  uint64_t out;
+};
+void launch_fnv_lanes(const fnv_lane_obj* d_objs, uint32_t n, uint64_t* out, cudaStream_t st);
+
 int sm_count(int device);
 unsigned long long launches();
 void count_launch();

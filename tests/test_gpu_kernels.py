@@ -142,3 +142,34 @@ def test_fnv_device_matches_oracle(gpu, native, oracle):
     f = torch.full((70_000,), 255, dtype=torch.uint8, device=gpu)
     assert api.fnv1a64_device([z, f]) == [oracle.fnv1a64(np.zeros(70_000, np.uint8)),
                                            oracle.fnv1a64(np.full(70_000, 255, np.uint8))]
+
+
+def test_fnv_lane_kernel_matches_oracle(gpu, native, oracle):
+    """Lane-serial FNV-1a kernel (one lane per object chain, 4-stage register
+    pipeline of 64-B blocks) == the serial byte chain: every block-pipeline
+    remainder (0-3 blocks, 0-3 vectors, 0-15 bytes), misaligned heads,
+    chaining, degenerate inputs, and many lanes of unequal lengths at once."""
+    from paper_2601_16956_b200 import api
+
+    rng = np.random.default_rng(11)
+    buf = torch.randint(0, 256, (12 << 20,), dtype=torch.uint8, device=gpu)
+    host = buf.cpu().numpy()
+    sizes = [0, 1, 15, 16, 17, 63, 64, 65, 127, 128, 191, 192, 255, 256, 257, 319, 320, 511, 512, 1023]
+    sizes += [64 * k + r for k in range(1, 9) for r in (0, 7, 16, 48, 63)]
+    sizes += [100_000, 3 << 20, (5 << 20) + 3]
+    sizes += [int(x) for x in rng.integers(1, 300_000, 70)]
+    views, exp = [], []
+    for s in sizes:
+        off = int(rng.integers(0, (12 << 20) - s - 1))
+        views.append(buf[off:off + s])
+        exp.append(oracle.fnv1a64(host[off:off + s]))
+    assert api.fnv1a64_device(views, lanes=True) == exp
+    assert api.fnv1a64_device(views[:1], lanes=True) == exp[:1]
+    full = buf[5:5 + 1_000_003]
+    a, b = full[:400_001], full[400_001:]
+    ha = api.fnv1a64_device([a], lanes=True)[0]
+    assert api.fnv1a64_device([b], init=[ha], lanes=True) == [oracle.fnv1a64(host[5:5 + 1_000_003])]
+    z = torch.zeros(70_000, dtype=torch.uint8, device=gpu)
+    f = torch.full((70_000,), 255, dtype=torch.uint8, device=gpu)
+    assert api.fnv1a64_device([z, f], lanes=True) == [oracle.fnv1a64(np.zeros(70_000, np.uint8)),
+                                                      oracle.fnv1a64(np.full(70_000, 255, np.uint8))]

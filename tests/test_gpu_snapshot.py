@@ -305,3 +305,26 @@ def test_bounded_enqueue_many_windows(gpu, tmp_path, mode):
     eng.shutdown()
     rs = api.restore_checkpoint(str(tmp_path / "c" / "MANIFEST.tlv"))
     assert torch.equal(rs[0].objects[0].payload.cuda(), x)
+
+
+@pytest.mark.parametrize("lane_max", [0, 4096, 1 << 40])
+@pytest.mark.parametrize("staging", [256 << 10, 64 << 20])  # ring of slots / full device shadow
+@pytest.mark.parametrize("name", ["hand_mixed", "odd_layout", "zero3_tiny", "two_ranks", "tiny_layout"])
+def test_lane_checksums_identical(gpu, tmp_path, name, staging, lane_max):
+    """Device checksums by the lane-serial FNV kernel over the state (objects up
+    to checksum_lane_max_bytes) next to the segment-parallel kernels over the
+    ring slots: same bytes as the reference; the lane share is reported."""
+    rec = S.load_recipe(os.path.join(GOLDEN, "recipes", name + ".recipe"))
+    out = str(tmp_path / "ckpt")
+    _, states, stats, _ = checkpoint_recipe(
+        rec, out, cfg_for("ring", checksum_lane_max_bytes=lane_max, checksum_host_frac=0.0,
+                          device_staging_bytes=staging))
+    assert read_tree(out) == read_tree(os.path.join(GOLDEN, "trees", name))
+    for st in states:
+        assert api.pattern_mismatches(st, rec.pit) == 0
+    dev = [o.size for r in rec.ranks for o in r.objects if o.kind == 0 and o.tier == 0]
+    lane = sum(s["lane_checksum_bytes"] for s in stats)
+    want = sum(x for x in dev if x <= lane_max)
+    assert lane == want
+    if lane:
+        assert all(s["lane_ms"] > 0 for s in stats if s["lane_checksum_bytes"])
