@@ -1203,8 +1203,9 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     // RING: the completer learns about the results only after the last
     // window, so it never blocks on the checksums ahead of windows whose
     // landing the bounded enqueue is waiting for
-    if (use_ring) fnv_publish = true;
-    else publish_fnv();
+    // (DIRECT / ZEROCOPY publish once the copy stream waits on the event:
+    // the completer recycles fnv_ev as soon as it has synchronized on it)
+    fnv_publish = true;
   };
   cuda_check(cudaStreamWaitEvent(pack_stream_, t.ev_start, 0), "wait producer");
   cuda_check(cudaStreamWaitEvent(copy_stream_, t.ev_start, 0), "wait producer");
@@ -1231,6 +1232,8 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     launch_checksums(0, pack_stream_);
     // DIRECT captures on the copy stream: it must also cover the checksum reads.
     cuda_check(cudaStreamWaitEvent(copy_stream_, j->fnv_ev, 0), "wait checksums");
+    publish_fnv();
+    fnv_publish = false;
   }
   if (j->img == 0) {
     mark_capture(pack_stream_);

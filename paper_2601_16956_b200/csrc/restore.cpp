@@ -307,23 +307,30 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
     }
   }
 
-  // Pipeline: K pinned windows of W bytes. Reads of a window are cut in 16 MiB
-  // preads spread over the pool; the task finishing a window's last read
-  // enqueues its H2D + scatter-unpack (windows are independent, any order) and
-  // a stream callback frees the slot. Reads run up to K windows ahead.
-  // (large windows: fewer, longer unpack launches — 1 GiB: 90 % of the HBM
-  // roofline vs 82-85 % at 256 MiB; small restores keep small staging)
-  // Tuning knobs for experiments (defaults measured best, profiles/r2_restore_knobs.log):
-  // TS_RESTORE_WINDOWS (ring depth), TS_RESTORE_READ_MB (pread piece).
+  // Pipeline: K device windows of W bytes (one H2D target + scatter-unpack
+  // launch each; windows are independent, any order; a stream callback frees
+  // the slot) fed through a small pool of P pinned pieces of R bytes: each
+  // pool task preads one piece and enqueues its H2D at once, so the copy
+  // engine reads the piece while it is still in the host's last-level cache
+  // (PCIe reads are coherent) — two passes over host DRAM per byte instead of
+  // three when whole windows were staged first (tools/restore_stage_probe.cu:
+  // 51 GB/s with 32 x 4 MiB pieces vs 37-41 GB/s for 1 GiB windows,
+  // profiles/r2_restore_stage_probe.jsonl), and 128 MiB of pinned staging
+  // instead of K x W. (Large device windows: fewer, longer unpack launches —
+  // 1 GiB: 90 % of the HBM roofline vs 82-85 % at 256 MiB.)
+  // Knobs for experiments: TS_RESTORE_WINDOWS (device ring depth),
+  // TS_RESTORE_READ_MB (piece size R), TS_RESTORE_PIECES (P).
   const char* kw = std::getenv("TS_RESTORE_WINDOWS");
   const int K = std::max(2, std::min(8, kw ? std::atoi(kw) : 4));  // (slot_busy holds 8)
   const uint64_t W = std::min<uint64_t>(1ull << 30, std::max<uint64_t>(64ull << 20, align_up(img / K + 1, 2ull << 20)));
   const char* rp = std::getenv("TS_RESTORE_READ_MB");
-  const uint64_t read_piece = static_cast<uint64_t>(std::max(1, std::min(1024, rp ? std::atoi(rp) : 16))) << 20;
+  const uint64_t R = static_cast<uint64_t>(std::max(1, std::min(64, rp ? std::atoi(rp) : 4))) << 20;
+  const char* pp = std::getenv("TS_RESTORE_PIECES");
+  const int P = std::max(2, std::min(256, pp ? std::atoi(pp) : 32));
   // One restore at a time uses the rings: take the lock first and size them
   // under it, so a concurrent restore cannot reallocate them in between.
   std::lock_guard<std::mutex> stage_guard(g_stage_mu);
-  uint8_t* hring = pinned_stage(W * K);
+  uint8_t* hring = pinned_stage(R * P);
   rtrace("pinned stage", t_begin);
   uint8_t* dring = nullptr;
   dev::useg* d_usegs = nullptr;
@@ -471,52 +478,49 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
       S.err_oid = e.object_id;
     }
   };
-  // Window finished reading: host-tier pieces to their buffers, device part
-  // H2D + scatter-unpack, slot freed by a stream callback.
-  // `direct`: the window has bytes in page-locked files (copied from there,
-  // file segment by file segment, instead of from the pinned slot).
-  auto window_read = [&](uint64_t lo, uint64_t hi, int slot, bool direct) {
-    uint8_t* hs = hring + static_cast<uint64_t>(slot) * W;
-    auto pit = std::lower_bound(pieces.begin(), pieces.end(), lo,
+  // Host-tier objects' bytes of image range [a, b), found at `src` (image
+  // byte a), to their host buffers.
+  auto copy_host_tier = [&](uint64_t a0, uint64_t b0, const uint8_t* src) {
+    auto pit = std::lower_bound(pieces.begin(), pieces.end(), a0,
                                 [](const rpiece& p, uint64_t x) { return p.pos + p.len <= x; });
-    for (; pit != pieces.end() && pit->pos < hi; ++pit) {
+    for (; pit != pieces.end() && pit->pos < b0; ++pit) {
       const auto& o = objs[pit->obj];
       if (o.d->tier == TS_TIER_DEVICE) continue;
-      const uint64_t a = std::max(lo, pit->pos), b = std::min(hi, pit->pos + pit->len);
+      const uint64_t a = std::max(a0, pit->pos), b = std::min(b0, pit->pos + pit->len);
       if (b > a)
         std::memcpy(static_cast<uint8_t*>(const_cast<void*>(o.d->data)) + pit->obj_off + (a - pit->pos),
-                    direct ? host_src(a, lo, hs) : hs + (a - lo), b - a);
+                    src + (a - a0), b - a);
     }
-    std::lock_guard<std::mutex> g(cuda_mu);
-    uint8_t* ds = dring + static_cast<uint64_t>(slot) * W;
-    if (!direct) {
-      cuda_check(cudaMemcpyAsync(ds, hs, hi - lo, cudaMemcpyHostToDevice, st), "H2D window");
-    } else {
-      for (size_t k = 0; k < rc.files.size(); ++k) {
-        const uint64_t a = std::max(lo, file_img[k].first);
-        const uint64_t b = std::min(hi, file_img[k].first + file_img[k].second);
-        if (b > a)
-          cuda_check(cudaMemcpyAsync(ds + (a - lo), host_src(a, lo, hs), b - a, cudaMemcpyHostToDevice, st),
-                     "H2D window");
+  };
+  // Every byte of window [lo, hi) is on the device (its H2Ds enqueued): the
+  // scatter-unpack, the device checksums' turn, and the callback freeing the
+  // slot. Under cuda_mu. After a failure only the slot is freed.
+  auto window_done = [&](uint64_t lo, uint64_t hi, int slot) {
+    bool ok;
+    {
+      std::lock_guard<std::mutex> g(S.mu);
+      ok = S.err_status == TS_OK;
+    }
+    if (ok) {
+      uint8_t* ds = dring + static_cast<uint64_t>(slot) * W;
+      auto uit = std::lower_bound(usegs.begin(), usegs.end(), lo,
+                                  [](const dev::useg& u, uint64_t x) { return u.pos + u.len <= x; });
+      if (uit != usegs.end() && uit->pos < hi) {
+        const size_t ui = static_cast<size_t>(uit - usegs.begin());
+        cudaEvent_t u0 = nullptr, u1 = nullptr;
+        cudaEventCreate(&u0);
+        cudaEventCreate(&u1);
+        cudaEventRecord(u0, st);
+        dev::launch_unpack(d_usegs + ui, static_cast<uint32_t>(usegs.size() - ui), lo, hi, ds, ctas, 512, st);
+        cudaEventRecord(u1, st);
+        unpack_ev.emplace_back(u0, u1);
+        launches_a += 1;
+        cuda_check(cudaGetLastError(), "unpack launch");
+        win_unpacked[lo / W] = u1;
       }
+      win_ready[lo / W] = 1;
+      fnv_advance();
     }
-    auto uit = std::lower_bound(usegs.begin(), usegs.end(), lo,
-                                [](const dev::useg& u, uint64_t x) { return u.pos + u.len <= x; });
-    if (uit != usegs.end() && uit->pos < hi) {
-      const size_t ui = static_cast<size_t>(uit - usegs.begin());
-      cudaEvent_t u0 = nullptr, u1 = nullptr;
-      cudaEventCreate(&u0);
-      cudaEventCreate(&u1);
-      cudaEventRecord(u0, st);
-      dev::launch_unpack(d_usegs + ui, static_cast<uint32_t>(usegs.size() - ui), lo, hi, ds, ctas, 512, st);
-      cudaEventRecord(u1, st);
-      unpack_ev.emplace_back(u0, u1);
-      launches_a += 1;
-      cuda_check(cudaGetLastError(), "unpack launch");
-      win_unpacked[lo / W] = u1;
-    }
-    win_ready[lo / W] = 1;
-    fnv_advance();
     cuda_check(cudaLaunchHostFunc(st, [](void* a) {
                  auto* p = static_cast<host_cb_arg*>(a);
                  std::lock_guard<std::mutex> g(p->s->mu);
@@ -524,6 +528,30 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
                  p->s->cv.notify_all();
                }, &cb_args[slot]), "cudaLaunchHostFunc");
   };
+  struct wstate {
+    uint64_t lo, hi;
+    int slot;
+    std::atomic<int> left{0};
+  };
+  // One part of a window is on its way to the device; the last one finishes it.
+  auto part_done = [&](wstate& ws) {  // under cuda_mu
+    if (--ws.left == 0) window_done(ws.lo, ws.hi, ws.slot);
+  };
+  // Pinned pieces: piece i of the restore uses buffer i % P; its mutex is held
+  // from the pread to the H2D's event record, and the next user of the buffer
+  // waits for that H2D.
+  std::vector<std::mutex> pmu(P);
+  std::vector<cudaEvent_t> pev(P, nullptr);
+  std::vector<char> pused(P, 0);
+  struct pev_guard {
+    std::vector<cudaEvent_t>& v;
+    ~pev_guard() {
+      for (auto e : v)
+        if (e) cudaEventDestroy(e);
+    }
+  } pev_g{pev};
+  for (auto& e : pev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  std::atomic<uint64_t> piece_seq{0};
 
   double read_s = 0;
   rtrace("setup done", t_begin);
@@ -540,66 +568,89 @@ void restore_handle::restore_rank(int index, const ts_object_desc* dst, size_t n
         if (S.err_status != TS_OK) break;
         S.slot_busy[slot] = 1;
       }
-      uint8_t* hs = hring + static_cast<uint64_t>(slot) * W;
-      struct wstate {
-        std::atomic<int> left{0};
-      };
       auto ws = std::make_shared<wstate>();
+      ws->lo = lo;
+      ws->hi = hi;
+      ws->slot = slot;
+      uint8_t* ds = dring + static_cast<uint64_t>(slot) * W;
       std::vector<std::tuple<size_t, uint64_t, uint64_t>> reads;
-      bool direct = false;
+      std::vector<std::pair<uint64_t, uint64_t>> direct;  // ranges in page-locked files
       for (size_t k = 0; k < rc.files.size(); ++k) {
         const uint64_t a = std::max(lo, file_img[k].first);
         const uint64_t b = std::min(hi, file_img[k].first + file_img[k].second);
-        if (b > a && regs.map[k]) {
-          direct = true;  // no pread: the copy engine reads the locked pages
+        if (b <= a) continue;
+        if (regs.map[k]) {  // no pread: the copy engine reads the locked pages
+          direct.push_back({a, b});
           continue;
         }
-        for (uint64_t x = a; x < b; x += read_piece) reads.emplace_back(k, x, std::min<uint64_t>(b, x + read_piece));
+        for (uint64_t x = a; x < b; x += R) reads.emplace_back(k, x, std::min<uint64_t>(b, x + R));
       }
-      if (reads.empty()) {
-        try {
-          window_read(lo, hi, slot, direct);
-        } catch (const error& e) {
-          set_err(e);
-          std::lock_guard<std::mutex> g(S.mu);
-          S.slot_busy[slot] = 0;
-          S.cv.notify_all();
-        }
-        continue;
-      }
-      ws->left = static_cast<int>(reads.size());
+      ws->left = static_cast<int>(reads.size()) + 1;  // + this thread's part (page-locked ranges)
       for (const auto& rd : reads) {
         const size_t k = std::get<0>(rd);
         const uint64_t x = std::get<1>(rd), y = std::get<2>(rd);
-        pool.submit([&, ws, k, x, y, lo, hi, slot, hs, direct] {
+        pool.submit([&, ws, k, x, y, ds] {
+          const int pi = static_cast<int>(piece_seq.fetch_add(1) % static_cast<uint64_t>(P));
           try {
-            read_range(fds[k], hs + (x - lo), y - x, header_reserved + (x - file_img[k].first), rc.files[k].path,
-                       &odirect_bytes);
+            std::lock_guard<std::mutex> pg(pmu[pi]);
+            if (pused[pi]) cuda_check(cudaEventSynchronize(pev[pi]), "restore piece");
+            uint8_t* hp = hring + static_cast<uint64_t>(pi) * R;
+            bool ok = true;
+            try {
+              read_range(fds[k], hp, y - x, header_reserved + (x - file_img[k].first), rc.files[k].path,
+                         &odirect_bytes);
+              copy_host_tier(x, y, hp);
+            } catch (const error& e) {
+              set_err(e);
+              ok = false;
+            }
+            std::lock_guard<std::mutex> g(cuda_mu);
+            try {
+              if (ok) {
+                cuda_check(cudaMemcpyAsync(ds + (x - ws->lo), hp, y - x, cudaMemcpyHostToDevice, st),
+                           "H2D piece");
+                cuda_check(cudaEventRecord(pev[pi], st), "event");
+                pused[pi] = 1;
+              }
+            } catch (const error& e) {
+              set_err(e);
+            }
+            part_done(*ws);
           } catch (const error& e) {
             set_err(e);
           }
-          if (--ws->left == 0) {
-            try {
-              window_read(lo, hi, slot, direct);
-            } catch (const error& e) {
-              set_err(e);
-              std::lock_guard<std::mutex> g(S.mu);
-              S.slot_busy[slot] = 0;
-              S.cv.notify_all();
-            }
-          }
         });
+      }
+      try {
+        for (const auto& [a, b] : direct) copy_host_tier(a, b, host_src(a, lo, nullptr));
+        std::lock_guard<std::mutex> g(cuda_mu);
+        try {
+          for (const auto& [a, b] : direct)
+            cuda_check(cudaMemcpyAsync(ds + (a - lo), host_src(a, lo, nullptr), b - a, cudaMemcpyHostToDevice, st),
+                       "H2D window");
+        } catch (const error& e) {
+          set_err(e);
+        }
+        part_done(*ws);
+      } catch (const error& e) {
+        set_err(e);
       }
     }
   }  // pool joins: every read done, every window enqueued
   {
     std::unique_lock<std::mutex> g(S.mu);
-    S.cv.wait(g, [&] {
-      for (int k = 0; k < K; ++k)
-        if (S.slot_busy[k]) return false;
-      return true;
-    });
+    if (S.err_status == TS_OK) {
+      S.cv.wait(g, [&] {
+        if (S.err_status != TS_OK) return true;
+        for (int k = 0; k < K; ++k)
+          if (S.slot_busy[k]) return false;
+        return true;
+      });
+    }
   }
+  // (after a failure a window may never have been finished: drain the stream
+  // so no copy still targets the staging)
+  cudaStreamSynchronize(st);
   read_s = (now_ns() - r0) * 1e-9;
   uint32_t launches = launches_a.load();
   // Host-tier destinations: checksums over the restored host buffers, 4 chains per core.
