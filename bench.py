@@ -476,6 +476,9 @@ def ours(args):
     image = stats[0]["image_bytes"]
     hbm_peak, peak_kind = peaks()
     pack_alg = raw + image  # read every raw byte, write the image (incl. alignment gaps)
+    packed = statistics.mean(s["packed_bytes"] for s in stats)
+    if 0 < packed < image:  # HYBRID: the pack kernels handle the last ring-full only
+        pack_alg = pack_alg * packed / image
     pack_mean = statistics.mean(pack_ms)
     # restore (one, after the loop): files written by the e2e phase below
     # --- e2e through the public API with files on /dev/shm -------------------
@@ -633,7 +636,9 @@ def ours(args):
     # a multi-slot HBM ring (cfg4) packs every chunk with the warp kernel
     pack_used = "bulk" if ((shadow and args.pack_kernel != "warp") or args.pack_kernel == "bulk-ring") else "warp"
     pack_label = ("copy-engine DMA" if args.mode == "direct" else
-                  "pack_bulk_kernel (TMA) + pack_kernel" if pack_used == "bulk" else "pack_kernel (warp gather)")
+                  "pack_bulk_kernel (TMA) + pack_kernel" if pack_used == "bulk" else
+                  "pack_kernel (warp gather; last ring-full only, the head leaves by copy-engine DMA)"
+                  if args.mode == "hybrid" else "pack_kernel (warp gather)")
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:  # (N=1 only)
         r = run_reference(args.config, 1, 3, 1, args.cpu_budget_s)
@@ -888,7 +893,7 @@ def main():
     ap.add_argument("--config", default="cfg4",
                     help="BASELINE.json workload: cfg4 (70B ZeRO-3 shard, the north-star config, default), "
                          "cfg1, cfg1b, cfg2, cfg3")
-    ap.add_argument("--mode", default="ring", choices=["ring", "direct", "zerocopy"])
+    ap.add_argument("--mode", default="ring", choices=["ring", "direct", "zerocopy", "hybrid"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--train-steps", type=int, default=8,
                     help="timed steps per off/lazy block (rounded up to whole checkpoint cycles)")

@@ -63,7 +63,10 @@ enum { TS_STRATEGY_SYNC = 0, TS_STRATEGY_TWO_PHASE = 1, TS_STRATEGY_LAZY = 2 };
  *  RING     gather-pack kernel into a bounded HBM staging ring, copy-engine D2H per window
  *  DIRECT   one copy-engine D2H per fragment straight from the state tensors
  *  ZEROCOPY gather-pack kernel storing straight into mapped pinned host memory
- *  HYBRID   DIRECT for fragments >= hybrid_direct_min_bytes, RING for the rest */
+ *  HYBRID   RING whose image exceeds the ring: the last ring-full is packed into the ring at
+ *           issue, the head leaves by copy-engine DMA per fragment piece straight from the
+ *           state (same capture point, the SMs pack a ring-full instead of the image); a full
+ *           device shadow is plain RING */
 enum { TS_D2H_RING = 0, TS_D2H_DIRECT = 1, TS_D2H_ZEROCOPY = 2, TS_D2H_HYBRID = 3 };
 
 /* ------------------------------------------------------------------------ */
@@ -160,7 +163,7 @@ typedef struct ts_engine_config {
   /* B200 knobs */
   int32_t d2h_mode;                 /* TS_D2H_*, default RING */
   uint64_t device_staging_bytes;    /* HBM staging ring; >= image bytes => full device shadow */
-  uint64_t hybrid_direct_min_bytes; /* HYBRID threshold */
+  uint64_t hybrid_direct_min_bytes; /* unused (kept for the ABI) */
   int32_t pack_ctas;                /* 0 = auto (one per SM) */
   int32_t pack_threads;             /* threads per pack CTA, default 512 */
   int32_t pack_priority;            /* capture (pack + checksum) stream priority: 1 highest (default:
@@ -316,6 +319,8 @@ typedef struct ts_ticket_stats {
   uint64_t lane_checksum_bytes; /* device-tier bytes hashed by the lane-serial FNV kernel */
   float lane_ms;                /* CUDA-event time of the lane-serial FNV kernel */
   uint32_t _pad5;
+  uint64_t packed_bytes;        /* image bytes written into the HBM ring by the pack kernels
+                                   (RING: the image; HYBRID: the last ring-full; other modes 0) */
 } ts_ticket_stats;
 ts_status ts_ticket_stats_get(ts_ticket* t, ts_ticket_stats* out);
 /* Per-object checksum accumulated at staging (transfer.cpp:163-166) */

@@ -124,7 +124,7 @@ class TicketStats(C.Structure):
                 ("failed", C.c_int32), ("file_dma_bytes", C.c_uint64),
                 ("host_checksum_bytes", C.c_uint64), ("helper_bytes", C.c_uint64),
                 ("direct_io_bytes", C.c_uint64), ("lane_checksum_bytes", C.c_uint64), ("lane_ms", C.c_float),
-                ("_pad5", C.c_uint32)]
+                ("_pad5", C.c_uint32), ("packed_bytes", C.c_uint64)]
 
 
 class RestoreObject(C.Structure):

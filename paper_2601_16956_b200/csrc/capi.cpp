@@ -377,6 +377,7 @@ ts_status ts_ticket_stats_get(ts_ticket* t, ts_ticket_stats* o) {
     o->direct_io_bytes = s.direct_io_bytes;
     o->lane_checksum_bytes = s.lane_checksum_bytes;
     o->lane_ms = s.lane_ms;
+    o->packed_bytes = s.packed_bytes;
   });
 }
 

@@ -1026,6 +1026,14 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     ring = ensure_device_ring(nslots == 1 ? want : nslots * chunk);
   }
   const bool use_ring = ring != nullptr;
+  // HYBRID (multi-slot ring): only the last ring-full is packed — into its
+  // own slots, at issue; the head chunks [0, H) leave the device straight
+  // from the state by copy-engine DMA per fragment piece. The capture
+  // completes at the same point as with the ring (all but the last ring-full
+  // has left the device) but the SMs pack a ring-full instead of the image.
+  const size_t H = (cfg_.d2h_mode == TS_D2H_HYBRID && use_ring && nslots > 1 && nchunks > nslots)
+                       ? nchunks - nslots : 0;
+  auto slot_of = [&](size_t c) -> uint8_t* { return ring + (nslots == 1 ? 0 : ((c - H) % nslots) * chunk); };
 
   // TMA bulk jobs (pack_kernel = 1, RING only): large 16-B aligned device
   // fragments are cut at absolute kBulkJob boundaries of the image (so no job
@@ -1128,7 +1136,8 @@ void engine::run_job(const std::shared_ptr<job>& j) {
           if (!lane_q.empty() && lane_q[q]) continue;
           const auto& r = j->raws[j->fnv_objs[q]];
           const uint64_t a = std::max(clo, r.img), b = std::min(chi, r.img + r.size);
-          fo.push_back({ring + (nslots == 1 ? 0 : (c % nslots) * chunk) + (a - clo), b - a, 0, 0, q});
+          // (head chunks of HYBRID: checksums over the state itself)
+          fo.push_back({c < H ? r.src + (a - r.img) : slot_of(c) + (a - clo), b - a, 0, 0, q});
         }
       }
       cbeg.push_back(fo.size());
@@ -1259,14 +1268,39 @@ void engine::run_job(const std::shared_ptr<job>& j) {
     std::vector<cudaEvent_t> packed_ev(nchunks, nullptr);
     cuda_check(cudaEventRecord(t.ev_d2h_first, copy_stream_), "event");
 
+    // Device checksums of chunk c over its ring slot, on the checksum stream,
+    // overlapping the D2H.
+    auto enqueue_checksums = [&](size_t c) {
+      {
+        // chunks whose slot is packed again in this job: capture path, pack
+        // priority; the last ring-full: low priority (chained states keep the
+        // launches in chunk order across the two streams)
+        const bool reused = c + nslots < nchunks;
+        cudaStream_t cs = reused ? ck_hi_stream_ : ck_stream_;
+        if (!reused && c > 0 && c - 1 + nslots < nchunks) {  // first low-priority chunk after high ones
+          cudaEvent_t hand;
+          cuda_check(cudaEventCreateWithFlags(&hand, cudaEventDisableTiming), "event");
+          cuda_check(cudaEventRecord(hand, ck_hi_stream_), "event");
+          cuda_check(cudaStreamWaitEvent(ck_stream_, hand, 0), "checksum order");
+          cudaEventDestroy(hand);
+        }
+        cuda_check(cudaStreamWaitEvent(cs, packed_ev[c], 0), "wait pack");
+        launch_checksums(c, cs);
+        cudaEvent_t ck;
+        cuda_check(cudaEventCreateWithFlags(&ck, cudaEventDisableTiming), "event");
+        cuda_check(cudaEventRecord(ck, cs), "event");
+        j->ck_events[c] = ck;
+      }
+    };
+
     // Pack of chunk c (+ its host-tier bytes and device checksums). Enqueued as
     // soon as the slot's previous chunk has its D2H and checksums enqueued, so
     // packs run up to a ring-full ahead of the window copies; the GPU-side
     // waits order them after the slot is free.
     auto enqueue_pack = [&](size_t c) {
       const uint64_t clo = c * chunk, chi = std::min(j->img, clo + chunk);
-      uint8_t* slot = ring + (shadow ? 0 : (c % nslots) * chunk);
-      if (c >= nslots) {  // the slot's previous chunk must have left the device and been checksummed
+      uint8_t* slot = slot_of(c);
+      if (c >= nslots + H) {  // the slot's previous chunk must have left the device and been checksummed
         cuda_check(cudaStreamWaitEvent(pack_stream_, j->chunk_events[c - nslots], 0), "slot wait");
         if (nf) cuda_check(cudaStreamWaitEvent(pack_stream_, j->ck_events[c - nslots], 0), "slot wait");
       }
@@ -1275,7 +1309,7 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       // shares the GPU with FNV kernels runs at 0.80 instead of 0.91 of the
       // HBM roofline). Low-priority checksums (the last ring-full) are never
       // waited for here: they must not delay the capture.
-      if (nf && c > 0 && c - 1 + nslots < nchunks && j->ck_events[c - 1])
+      if (nf && c > H && c - 1 + nslots < nchunks && j->ck_events[c - 1])
         cuda_check(cudaStreamWaitEvent(pack_stream_, j->ck_events[c - 1], 0), "pack after checksums");
       cudaEvent_t pa, pb;
       cuda_check(cudaEventCreate(&pa), "event");
@@ -1307,39 +1341,85 @@ void engine::run_job(const std::shared_ptr<job>& j) {
       cuda_check(cudaGetLastError(), "pack kernel launch");
       cuda_check(cudaEventCreateWithFlags(&packed_ev[c], cudaEventDisableTiming), "event");
       cuda_check(cudaEventRecord(packed_ev[c], pack_stream_), "event");
-      if (c + 1 == nchunks) {
+      if (c + 1 == nchunks && H == 0) {  // (HYBRID: after the head's copies, below)
         // the lane checksums read the state: the capture covers them
         if (j->lane_ev1) cuda_check(cudaStreamWaitEvent(pack_stream_, j->lane_ev1, 0), "capture after lanes");
         mark_capture(pack_stream_);
       }
-      if (nf) {  // reads the slot on the checksum stream, overlapping the D2H
-        // chunks whose slot is packed again in this job: capture path, pack
-        // priority; the last ring-full: low priority (chained states keep the
-        // launches in chunk order across the two streams)
-        const bool reused = c + nslots < nchunks;
-        cudaStream_t cs = reused ? ck_hi_stream_ : ck_stream_;
-        if (!reused && c > 0 && c - 1 + nslots < nchunks) {  // first low-priority chunk after high ones
-          cudaEvent_t hand;
-          cuda_check(cudaEventCreateWithFlags(&hand, cudaEventDisableTiming), "event");
-          cuda_check(cudaEventRecord(hand, ck_hi_stream_), "event");
-          cuda_check(cudaStreamWaitEvent(ck_stream_, hand, 0), "checksum order");
-          cudaEventDestroy(hand);
-        }
-        cuda_check(cudaStreamWaitEvent(cs, packed_ev[c], 0), "wait pack");
-        launch_checksums(c, cs);
-        cudaEvent_t ck;
-        cuda_check(cudaEventCreateWithFlags(&ck, cudaEventDisableTiming), "event");
-        cuda_check(cudaEventRecord(ck, cs), "event");
-        j->ck_events[c] = ck;
-      }
+      if (nf && !(H && c >= H)) enqueue_checksums(c);
     };
 
     size_t next_pack = 0;
+    t.packed_bytes = j->img - std::min<uint64_t>(j->img, H * chunk);
+    if (H) {
+      // HYBRID: the last ring-full is packed at once; then the head's
+      // checksums over the state (the capture waits for them: pack priority;
+      // after the packs, not beside them: a pack sharing the SMs with FNV
+      // kernels runs at ~0.55 instead of ~0.9 of the HBM roofline), then the
+      // tail's checksums over its slots (low priority, chained after the head).
+      for (size_t c = H; c < nchunks; ++c) enqueue_pack(c);
+      next_pack = nchunks;
+      if (nf) {
+        cudaEvent_t ready;
+        cuda_check(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
+        cuda_check(cudaEventRecord(ready, pack_stream_), "event");  // tables uploaded, producer done, tail packed
+        cuda_check(cudaStreamWaitEvent(ck_hi_stream_, ready, 0), "head checksums wait");
+        cudaEventDestroy(ready);
+        for (size_t c = 0; c < H; ++c) {
+          launch_checksums(c, ck_hi_stream_);
+          cudaEvent_t ck;
+          cuda_check(cudaEventCreateWithFlags(&ck, cudaEventDisableTiming), "event");
+          cuda_check(cudaEventRecord(ck, ck_hi_stream_), "event");
+          j->ck_events[c] = ck;
+        }
+        for (size_t c = H; c < nchunks; ++c) enqueue_checksums(c);
+      }
+    }
     for (size_t c = 0; c < nchunks && !failed(); ++c) {
       while (next_pack < nchunks && (next_pack < nslots || j->chunk_events[next_pack - nslots] != nullptr))
         enqueue_pack(next_pack++);
+      if (c < H) {  // HYBRID head: copy-engine DMA per fragment piece, gaps zeroed on the host
+        for (size_t q = cw0[c]; q < cw0[c + 1] && !failed(); ++q) {
+          auto& win = j->wins[q];
+          throttle();
+          acquire(win);
+          uint8_t* dst = win.host;
+          size_t k = std::upper_bound(j->segs.begin(), j->segs.end(), win.lo,
+                                      [](uint64_t x, const dev::seg& sg) { return x < sg.pos; }) - j->segs.begin();
+          k = k ? k - 1 : 0;
+          for (size_t qq = k; qq < j->segs.size() && j->segs[qq].pos < win.hi; ++qq) {
+            const auto& sg = j->segs[qq];
+            const uint64_t a = std::max(win.lo, sg.pos), b = std::min(win.hi, sg.pos + sg.len);
+            if (b <= a) continue;
+            if (sg.src) {
+              cuda_check(cudaMemcpyAsync(dst + (a - win.lo), sg.src + (a - sg.pos), b - a, cudaMemcpyDeviceToHost,
+                                         copy_stream_), "D2H fragment");
+              t.copies += 1;
+            } else {
+              std::memset(dst + (a - win.lo), 0, b - a);
+            }
+          }
+          for (uint32_t hk = win.hp_begin; hk < win.hp_end; ++hk)  // host-tier bytes, in stream order (capture)
+            cuda_check(cudaMemcpyAsync(dst + j->hp[hk].win_off, j->hp[hk].src, j->hp[hk].len,
+                                       cudaMemcpyHostToHost, copy_stream_), "host-tier bytes to the window");
+          seen_bytes += win.hi - win.lo;
+          cuda_check(cudaEventRecord(win.ev, copy_stream_), "event");
+          push_window(q);
+        }
+        cudaEvent_t done;
+        cuda_check(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "event");
+        cuda_check(cudaEventRecord(done, copy_stream_), "event");
+        j->chunk_events[c] = done;
+        if (c + 1 == H) {  // the state may change once the head has left and the tail is packed
+          cuda_check(cudaStreamWaitEvent(pack_stream_, done, 0), "capture after the head");
+          if (nf) cuda_check(cudaStreamWaitEvent(pack_stream_, j->ck_events[H - 1], 0), "capture after the head");
+          if (j->lane_ev1) cuda_check(cudaStreamWaitEvent(pack_stream_, j->lane_ev1, 0), "capture after lanes");
+          mark_capture(pack_stream_);
+        }
+        continue;
+      }
       const uint64_t clo = c * chunk;
-      uint8_t* slot = ring + (shadow ? 0 : (c % nslots) * chunk);
+      uint8_t* slot = slot_of(c);
       cuda_check(cudaStreamWaitEvent(copy_stream_, packed_ev[c], 0), "wait pack");
       std::vector<char> helper_used(helpers_.size(), 0);
       for (size_t q = cw0[c]; q < cw0[c + 1]; ++q) {

@@ -105,6 +105,7 @@ struct ticket_state {
   uint64_t direct_io_bytes = 0;      // fixed-region bytes written O_DIRECT (flush_mmap = 2)
   float pack_ms = 0, d2h_ms = 0, lane_ms = 0;
   uint64_t lane_checksum_bytes = 0;  // device-tier bytes hashed by the lane-serial FNV kernel
+  uint64_t packed_bytes = 0;         // image bytes written by the pack kernels
   uint32_t kernel_launches = 0, copies = 0;
   cudaEvent_t ev_start = nullptr, ev_capture = nullptr, ev_d2h_first = nullptr,
               ev_d2h_last = nullptr, ev_pack0 = nullptr;

@@ -16,7 +16,7 @@ from paper_2601_16956_b200 import api
 from paper_2601_16956_b200 import synthetic as S
 
 pytestmark = pytest.mark.gpu
-MODES = ["ring", "direct", "zerocopy", "ring-bulk"]
+MODES = ["ring", "direct", "zerocopy", "ring-bulk", "hybrid"]
 
 
 def cfg_for(mode, **kw):
@@ -210,7 +210,7 @@ def test_retired_checkpoint_is_not_restorable(gpu, tmp_path):
 
 
 @pytest.mark.parametrize("frac", [0.0, 0.3, 0.5, 1.0])
-@pytest.mark.parametrize("mode", ["ring", "direct", "zerocopy"])
+@pytest.mark.parametrize("mode", ["ring", "direct", "zerocopy", "hybrid"])
 @pytest.mark.parametrize("name", ["hand_mixed", "zero3_tiny", "two_ranks"])
 def test_checksum_split_identical(gpu, tmp_path, name, mode, frac):
     """Checksum placement split between the FNV kernels and host workers
@@ -307,17 +307,18 @@ def test_bounded_enqueue_many_windows(gpu, tmp_path, mode):
     assert torch.equal(rs[0].objects[0].payload.cuda(), x)
 
 
+@pytest.mark.parametrize("mode", ["ring", "hybrid"])
 @pytest.mark.parametrize("lane_max", [0, 4096, 1 << 40])
 @pytest.mark.parametrize("staging", [256 << 10, 64 << 20])  # ring of slots / full device shadow
 @pytest.mark.parametrize("name", ["hand_mixed", "odd_layout", "zero3_tiny", "two_ranks", "tiny_layout"])
-def test_lane_checksums_identical(gpu, tmp_path, name, staging, lane_max):
+def test_lane_checksums_identical(gpu, tmp_path, name, staging, lane_max, mode):
     """Device checksums by the lane-serial FNV kernel over the state (objects up
     to checksum_lane_max_bytes) next to the segment-parallel kernels over the
     ring slots: same bytes as the reference; the lane share is reported."""
     rec = S.load_recipe(os.path.join(GOLDEN, "recipes", name + ".recipe"))
     out = str(tmp_path / "ckpt")
     _, states, stats, _ = checkpoint_recipe(
-        rec, out, cfg_for("ring", checksum_lane_max_bytes=lane_max, checksum_host_frac=0.0,
+        rec, out, cfg_for(mode, checksum_lane_max_bytes=lane_max, checksum_host_frac=0.0,
                           device_staging_bytes=staging))
     assert read_tree(out) == read_tree(os.path.join(GOLDEN, "trees", name))
     for st in states:
