@@ -100,7 +100,7 @@ def ncu_traffic(cfg: str, mode: str, pack_kernel: str):
     except Exception:
         return None
     for e in t.get("entries", [t]):
-        if e.get("workload") == cfg and mode == "ring" and pack_kernel == e.get("pack_kernel", "warp"):
+        if e.get("workload") == cfg and mode == e.get("mode", "ring") and pack_kernel == e.get("pack_kernel", "warp"):
             return int(e["traffic_bytes_per_launch"])
     return None
 
@@ -893,7 +893,7 @@ def main():
     ap.add_argument("--config", default="cfg4",
                     help="BASELINE.json workload: cfg4 (70B ZeRO-3 shard, the north-star config, default), "
                          "cfg1, cfg1b, cfg2, cfg3")
-    ap.add_argument("--mode", default="ring", choices=["ring", "direct", "zerocopy", "hybrid"])
+    ap.add_argument("--mode", default="hybrid", choices=["ring", "direct", "zerocopy", "hybrid"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--train-steps", type=int, default=8,
                     help="timed steps per off/lazy block (rounded up to whole checkpoint cycles)")

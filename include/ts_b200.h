@@ -161,9 +161,10 @@ typedef struct ts_engine_config {
   int64_t cache_acquire_timeout_ns; /* < 0: wait forever; default 300 s (engine.hpp:50) */
   int32_t overwrite;                /* default 1 */
   /* B200 knobs */
-  int32_t d2h_mode;                 /* TS_D2H_*, default RING */
+  int32_t d2h_mode;                 /* TS_D2H_*, default HYBRID (= RING for a full device shadow) */
   uint64_t device_staging_bytes;    /* HBM staging ring; >= image bytes => full device shadow */
-  uint64_t hybrid_direct_min_bytes; /* unused (kept for the ABI) */
+  uint64_t hybrid_direct_min_bytes; /* HYBRID: the head goes by DMA only when its mean fragment
+                                       piece is at least this (default 1 MiB); else plain RING */
   int32_t pack_ctas;                /* 0 = auto (one per SM) */
   int32_t pack_threads;             /* threads per pack CTA, default 512 */
   int32_t pack_priority;            /* capture (pack + checksum) stream priority: 1 highest (default:

@@ -337,9 +337,9 @@ class EngineConfig:
     cache_acquire_timeout_ns: Optional[int] = 300 * 10**9
     overwrite: bool = True
     # B200 knobs
-    d2h_mode: str = "ring"
+    d2h_mode: str = "hybrid"  # = ring when the image fits the device staging (full shadow)
     device_staging_bytes: int = 2 << 30
-    hybrid_direct_min_bytes: int = 64 << 20
+    hybrid_direct_min_bytes: int = 1 << 20  # HYBRID head only if its mean fragment piece is >= this
     pack_ctas: int = 0
     pack_threads: int = 512
     pack_priority: int = 1  # capture stream: 1 high (default), 0 normal, -1 low

@@ -188,9 +188,9 @@ void ts_engine_config_default(ts_engine_config* c) {
   c->alignment = 4096;
   c->cache_acquire_timeout_ns = 300ll * 1000000000ll;
   c->overwrite = 1;
-  c->d2h_mode = TS_D2H_RING;
+  c->d2h_mode = TS_D2H_HYBRID;
   c->device_staging_bytes = 2ull << 30;
-  c->hybrid_direct_min_bytes = 64ull << 20;
+  c->hybrid_direct_min_bytes = 1ull << 20;
   c->pack_ctas = 0;
   c->pack_threads = 512;
   c->pack_priority = 1;

@@ -1031,8 +1031,19 @@ void engine::run_job(const std::shared_ptr<job>& j) {
   // from the state by copy-engine DMA per fragment piece. The capture
   // completes at the same point as with the ring (all but the last ring-full
   // has left the device) but the SMs pack a ring-full instead of the image.
-  const size_t H = (cfg_.d2h_mode == TS_D2H_HYBRID && use_ring && nslots > 1 && nchunks > nslots)
-                       ? nchunks - nslots : 0;
+  // Only for large fragments: the head costs one DMA per fragment piece
+  // (hybrid_direct_min_bytes: the least mean piece size, default 1 MiB).
+  size_t H = (cfg_.d2h_mode == TS_D2H_HYBRID && use_ring && nslots > 1 && nchunks > nslots) ? nchunks - nslots : 0;
+  if (H) {
+    uint64_t hb = 0, np = 0;
+    for (const auto& sg : j->segs) {
+      if (sg.pos >= H * chunk) break;
+      if (!sg.src) continue;
+      hb += std::min<uint64_t>(sg.len, H * chunk - sg.pos);
+      ++np;
+    }
+    if (np == 0 || hb / np < cfg_.hybrid_direct_min_bytes) H = 0;
+  }
   auto slot_of = [&](size_t c) -> uint8_t* { return ring + (nslots == 1 ? 0 : ((c - H) % nslots) * chunk); };
 
   // TMA bulk jobs (pack_kernel = 1, RING only): large 16-B aligned device

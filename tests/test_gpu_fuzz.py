@@ -41,14 +41,15 @@ def random_recipe(rng: random.Random) -> S.Recipe:
 
 
 def random_cfg(rng):
-    mode = rng.choice(["ring", "direct", "zerocopy"])
+    mode = rng.choice(["ring", "direct", "zerocopy", "hybrid"])
     w = rng.choice([4096, 10_000, 65536, 1 << 20])
     return api.EngineConfig(
         d2h_mode=mode, raw_chunk_bytes=w, staging_capacity_bytes=rng.choice([w, 2 * w + 7, 8 << 20]),
         device_staging_bytes=rng.choice([8192, 1 << 16, 1 << 24]), flush_workers=rng.choice([1, 2, 5]),
         checksum_on_gpu=rng.random() < 0.7, flush_mmap=rng.choice([0, 1, 1, 2]),
         pack_kernel=rng.choice(["warp", "bulk"]), bulk_min_bytes=32768,
-        serialized_chunk_bytes=rng.choice([1 << 20, 1 << 20, 4096]))
+        serialized_chunk_bytes=rng.choice([1 << 20, 1 << 20, 4096]),
+        hybrid_direct_min_bytes=0)  # (the HYBRID head path even for tiny fragments)
 
 
 @pytest.mark.parametrize("seed", range(40))

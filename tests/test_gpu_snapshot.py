@@ -24,6 +24,8 @@ def cfg_for(mode, **kw):
     if mode == "ring-bulk":  # TMA bulk copies for every fragment >= 32 KiB
         # (a full device shadow: the bulk path is used for one-pack images only)
         mode, extra = "ring", dict(pack_kernel="bulk", bulk_min_bytes=32768, device_staging_bytes=256 << 20)
+    elif mode == "hybrid":  # the head path even for the goldens' KiB-sized fragments
+        extra = dict(hybrid_direct_min_bytes=0)
     base = dict(d2h_mode=mode, raw_chunk_bytes=64 << 10, staging_capacity_bytes=1 << 20,
                 device_staging_bytes=256 << 10, flush_workers=3)
     base.update(extra)

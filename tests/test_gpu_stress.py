@@ -35,7 +35,7 @@ def test_lazy_loop_rotation_stress(gpu, shm, seed):
     spec = rec.ranks[0]
     cfg = random_cfg(rng)
     cfg.checksum_host_frac = rng.choice([-1.0, 0.0, 0.5, 1.0])
-    if cfg.d2h_mode == "ring" and rng.random() < 0.5:
+    if cfg.d2h_mode in ("ring", "hybrid") and rng.random() < 0.5:
         cfg.helper_devices, cfg.helper_share = (0,), rng.choice([0.25, 0.75])
     keep = rng.choice([1, 2])
     spare = os.path.join(shm, "spare")

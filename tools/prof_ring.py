@@ -16,11 +16,12 @@ from paper_2601_16956_b200 import api
 from paper_2601_16956_b200 import synthetic as S
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
+mode = sys.argv[2] if len(sys.argv) > 2 else "ring"  # "hybrid": only the last ring-full is packed
 spec = S.config_recipe(cfg, 0).ranks[0]
 st = api.materialize_payloads(spec, 0, 1)
 free, _ = torch.cuda.mem_get_info(0)
 ring = max(8 << 30, free - (26 << 30))
-ec = api.EngineConfig(staging_capacity_bytes=4 << 30, raw_chunk_bytes=64 << 20, device_staging_bytes=ring,
+ec = api.EngineConfig(d2h_mode=mode, staging_capacity_bytes=4 << 30, raw_chunk_bytes=64 << 20, device_staging_bytes=ring,
                       write_files=False, flush_workers=16)
 eng = api.CheckpointEngine(ec, 0, 0)
 for it in (2, 3):
@@ -29,6 +30,6 @@ for it in (2, 3):
     t = eng.issue_checkpoint(sess, st, it)
     t.wait_persisted()
     s = t.stats()
-    print(json.dumps({"config": cfg, "ring_bytes": ring, "image_bytes": s["image_bytes"], "raw_bytes": spec.raw_bytes,
+    print(json.dumps({"config": cfg, "mode": mode, "packed_bytes": s["packed_bytes"], "ring_bytes": ring, "image_bytes": s["image_bytes"], "raw_bytes": spec.raw_bytes,
                       "pack_ms": s["pack_ms"], "kernel_launches": s["kernel_launches"]}), flush=True)
 eng.shutdown()
