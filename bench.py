@@ -90,7 +90,7 @@ class Clocks:
                 "power_w": round(statistics.median(pw), 1) if pw else None}
 
 
-def ncu_traffic(cfg: str, mode: str, pack_kernel: str):
+def ncu_traffic(cfg: str, mode: str, pack_kernel: str, alg: float = 0.0):
     """DRAM bytes of the pack kernels of one checkpoint of this workload from
     the committed ncu capture (profiles/ncu_traffic.json: cfg2 full-shadow
     bulk+warp, cfg4 ring warp), else None."""
@@ -101,6 +101,8 @@ def ncu_traffic(cfg: str, mode: str, pack_kernel: str):
         return None
     for e in t.get("entries", [t]):
         if e.get("workload") == cfg and mode == e.get("mode", "ring") and pack_kernel == e.get("pack_kernel", "warp"):
+            if e.get("scale_with_alg") and alg:  # (captured with another ring size: same traffic per byte)
+                return int(alg * e["traffic_bytes_per_launch"] / e["alg_bytes_per_launch"])
             return int(e["traffic_bytes_per_launch"])
     return None
 
@@ -680,7 +682,7 @@ def ours(args):
                          "bound": "hbm", "achieved": round(pack_alg / (pack_mean / 1e3) / 1e9, 1),
                          "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(pack_alg / (pack_mean / 1e3) / 1e9 / hbm_peak, 3),
-                         "traffic": ncu_traffic(args.config, args.mode, pack_used),
+                         "traffic": ncu_traffic(args.config, args.mode, pack_used, pack_alg),
                          "traffic_source": "profiles/ncu_traffic.json (ncu --set full, same workload)",
                          "alg_bytes_per_launch": int(pack_alg),
                          "launch_ms": round(pack_mean, 3)},

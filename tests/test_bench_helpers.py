@@ -40,3 +40,6 @@ def test_ncu_traffic_lookup():
     assert t2 is not None and 0.99 < t2 / 47_169_153_216 < 1.01
     assert bench.ncu_traffic("cfg3", "ring", "warp") is None
     assert bench.ncu_traffic("cfg4", "direct", "warp") is None
+    # HYBRID: captured with another ring size, scaled per algorithmic byte
+    th = bench.ncu_traffic("cfg4", "hybrid", "warp", 68_680_618_388)
+    assert 0.99 * 68_680_618_388 < th < 68_680_618_388
