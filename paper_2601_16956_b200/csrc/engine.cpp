@@ -422,22 +422,36 @@ uint8_t* engine::ensure_device_ring(uint64_t bytes) {
   return ring_;
 }
 
+// The checksum scratch and the segment tables regrow when a job needs more
+// (the auto checksum placement changes the GPU share, hence the segment
+// length and count, from job to job). Stream-ordered on the pack stream,
+// where every earlier user of the old buffer is already ordered (run_job
+// orders each job after the previous one's checksums): a cudaFree there
+// would synchronize the whole device — wait out the training kernels — and
+// stall the training thread's own CUDA calls behind the driver for as long
+// (measured: one 795 ms cudaEventRecord in a lazy training block).
+// Headroom: 1.5x, so growth is rare.
 uint8_t* engine::ensure_fnv_buffer(uint64_t bytes) {
   if (fnvbuf_bytes_ < bytes) {
-    if (fnvbuf_) cudaFree(fnvbuf_);
+    const uint64_t want = std::max<uint64_t>(bytes + bytes / 2, 1ull << 20);
+    if (fnvbuf_) cuda_check(cudaFreeAsync(fnvbuf_, pack_stream_), "cudaFreeAsync(checksum scratch)");
     fnvbuf_ = nullptr;
-    cuda_check(cudaMalloc(&fnvbuf_, bytes), "cudaMalloc(checksum scratch)");
-    fnvbuf_bytes_ = bytes;
+    fnvbuf_bytes_ = 0;
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&fnvbuf_), want, pack_stream_),
+               "cudaMallocAsync(checksum scratch)");
+    fnvbuf_bytes_ = want;
   }
   return fnvbuf_;
 }
 
 void* engine::ensure_seg_buffer(uint64_t bytes) {
   if (segbuf_bytes_ < bytes) {
-    if (segbuf_) cudaFree(segbuf_);
+    const uint64_t want = std::max<uint64_t>(bytes + bytes / 2, 1ull << 20);
+    if (segbuf_) cuda_check(cudaFreeAsync(segbuf_, pack_stream_), "cudaFreeAsync(segment table)");
     segbuf_ = nullptr;
-    cuda_check(cudaMalloc(&segbuf_, bytes), "cudaMalloc(segment table)");
-    segbuf_bytes_ = bytes;
+    segbuf_bytes_ = 0;
+    cuda_check(cudaMallocAsync(&segbuf_, want, pack_stream_), "cudaMallocAsync(segment table)");
+    segbuf_bytes_ = want;
   }
   return segbuf_;
 }
@@ -1182,11 +1196,16 @@ void engine::run_job(const std::shared_ptr<job>& j) {
                                  cudaMemcpyHostToDevice, pack_stream_),
                  "upload lane checksum table");
     if (ck_host_n_ < nf) {  // the previous job's results were consumed before its snapshot completed
+      // (sized for every device-tier object, so a growing GPU share does not
+      // reallocate: cudaFreeHost synchronizes the device)
+      uint32_t ndev = 0;
+      for (const auto& r : j->raws) ndev += r.device ? 1 : 0;
       if (ck_host_) cudaFreeHost(ck_host_);
       ck_host_ = nullptr;
-      cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&ck_host_), nf * 8ull, cudaHostAllocMapped | cudaHostAllocPortable),
+      const uint32_t cap = std::max(nf, ndev);
+      cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&ck_host_), cap * 8ull, cudaHostAllocMapped | cudaHostAllocPortable),
                  "cudaHostAlloc(checksums)");
-      ck_host_n_ = nf;
+      ck_host_n_ = cap;
     }
     j->fnv_out = ck_host_;
     j->fnv_ev = get_event();
